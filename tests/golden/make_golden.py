@@ -1,0 +1,109 @@
+"""Generate golden fixtures from the *reference* symbolic front end.
+
+Run in the build container only (it imports /root/reference, which does not
+exist on the GPU box):
+
+    python tests/golden/make_golden.py
+
+Writes tests/golden/symbolics_golden.json: exact FD tables, the printed
+solved/CSE'd update equations (Appendix-B form) for every kernel family and
+space order the B200 path supports, and exact-rational evaluation probes.
+The product's own symbolics (paper_2312_13094_b200/symbolics.py) is checked
+against this file by tests/test_symbolics_golden.py.
+"""
+import hashlib
+import json
+import os
+import sys
+from fractions import Fraction
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "symbolics_golden.json")
+
+
+def case_equations(S, kind, ndims, so):
+    """Build the family's symbolic equation with module ``S`` (reference or
+    product: both expose the same API). Returns (eq, unknown)."""
+    shape = (4,) * ndims if kind == "diffusion" else (16,) * ndims
+    g = S.GridSpec(shape=shape, extent=(2.0,) * ndims)
+    if kind == "diffusion":
+        u = S.FieldSpec(name="u", grid=g, space_order=so, time_order=1)
+        return S.Eq(u.dt, u.laplace), u.forward
+    if kind == "acoustic":
+        u = S.FieldSpec(name="u", grid=g, space_order=so, time_order=2)
+        m = S.FieldSpec(name="m", grid=g, space_order=so, time_order=0)
+        return S.Eq(m.at() * u.dt2 - u.laplace), u.forward
+    if kind == "tti_gxx":
+        # G = D^T D with D = a_x d/dx + a_y d/dy + a_z d/dz,
+        # nested first derivatives; a_* are static direction-cosine fields.
+        u = S.FieldSpec(name="u", grid=g, space_order=so, time_order=2)
+        m = S.FieldSpec(name="m", grid=g, space_order=so, time_order=0)
+        a = [S.FieldSpec(name=f"a{S.AXIS_NAMES[i]}", grid=g, space_order=so,
+                         time_order=0) for i in range(3)]
+        inner = S.add(*(S.mul(a[j].at(), u.d(j)) for j in range(3)))
+        gxx = S.add(*(S.Deriv(S.mul(a[i].at(), inner), i, 1) for i in range(3)))
+        return S.Eq(m.at() * u.dt2 - gxx), u.forward
+    raise ValueError(kind)
+
+
+CASES = (
+    [("diffusion", 2, so) for so in (2, 4, 8)]
+    + [("diffusion", 3, so) for so in (2, 4)]
+    + [("acoustic", nd, so) for nd in (2, 3) for so in (2, 4, 8, 12, 16)]
+    + [("tti_gxx", 3, so) for so in (2, 4, 8)]
+)
+
+
+def probe(S, expr, seed):
+    """Exact evaluation on seeded rational bindings keyed by leaf text."""
+    import random
+    rng = random.Random(seed)
+    leaves = sorted({S.format_expr(n) for n in S.walk(expr)
+                     if isinstance(n, (S.Symbol, S.FieldAccess))})
+    vals = {k: Fraction(rng.randint(1, 40), rng.randint(1, 12)) for k in leaves}
+    bind = {n: vals[S.format_expr(n)] for n in S.walk(expr)
+            if isinstance(n, (S.Symbol, S.FieldAccess))}
+    return str(S.eval_exact(expr, bind))
+
+
+def describe(S, kind, nd, so):
+    eq, unknown = case_equations(S, kind, nd, so)
+    solved = S.solve_forward(eq, unknown)
+    cse = S.apply_cse(solved)
+    lines = S.format_equation(solved)
+    cse_lines = S.format_equation(cse)
+    offs = sorted({a.offsets for a in S.accesses(solved.rhs)})
+    text = "\n".join(lines)
+    cse_text = "\n".join(cse_lines)
+    rec = {
+        "kind": kind, "ndims": nd, "so": so,
+        "sha256": hashlib.sha256(text.encode()).hexdigest(),
+        "cse_sha256": hashlib.sha256(cse_text.encode()).hexdigest(),
+        "n_accesses": len(S.accesses(solved.rhs)),
+        "unique_offsets": len(offs),
+        "radius": max(abs(o) for off in offs for o in off),
+        "n_temporaries": len(cse.temporaries),
+        "probe": [probe(S, solved.rhs, s) for s in range(3)],
+    }
+    if len(text) < 4000:
+        rec["lines"] = lines
+        rec["cse_lines"] = cse_lines
+    return rec
+
+
+def main():
+    sys.path.insert(0, REF)
+    from stencil_dmp import symbolics as S
+    data = {
+        "generator": "tests/golden/make_golden.py (reference symbolics.py)",
+        "fd": {f"{d},{acc}": [str(c) for c in S.fd_coefficients(d, acc)]
+               for d in (1, 2) for acc in range(2, 18, 2)},
+        "cases": [describe(S, *c) for c in CASES],
+    }
+    with open(OUT, "w") as f:
+        json.dump(data, f, indent=1)
+    print("wrote", OUT, len(data["cases"]), "cases")
+
+
+if __name__ == "__main__":
+    main()
