@@ -1,0 +1,269 @@
+// Sparse injection / interpolation and halo data
+// movement (pack/unpack SPEC.md:430-438, box copies and completion flags
+// for the NVLink peer exchange that replaces the SPEC Transport,
+// SPEC.md:406-411) for sm_100a.
+#include "common.cuh"
+
+namespace sdmp {
+
+// ---- sparse --------------------------------------------------------------
+
+// One thread per owned grid node; contributions pre-sorted by point id on
+// the host, summed sequentially: deterministic, no float atomics.
+__global__ void k_inject(float* __restrict__ f, const int64_t* __restrict__ node,
+                         const int32_t* __restrict__ ptr, int nnodes,
+                         const int32_t* __restrict__ pid, const float* __restrict__ w,
+                         const float* __restrict__ amps, float C, const float* __restrict__ m) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= nnodes) return;
+  float acc = 0.f;
+  for (int j = ptr[n]; j < ptr[n + 1]; ++j) acc = __fmaf_rn(w[j], amps[pid[j]], acc);
+  const int64_t i = node[n];
+  const float s = m ? __fdiv_rn(C, m[i]) : C;
+  f[i] = __fmaf_rn(acc, s, f[i]);
+}
+
+__global__ void k_interp(const float* __restrict__ f, const int64_t* __restrict__ idx,
+                         const float* __restrict__ w, int npts, int nc, float* __restrict__ out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npts) return;
+  float acc = 0.f;
+  for (int c = 0; c < nc; ++c) acc = __fmaf_rn(w[p * nc + c], __ldg(f + idx[p * nc + c]), acc);
+  out[p] = acc;
+}
+
+int inject(cudaStream_t st, float* field, const int64_t* node, const int32_t* ptr, int nnodes,
+           const int32_t* pid, const float* w, const float* amps, float C, const float* m) {
+  if (nnodes <= 0) return SDMP_OK;
+  SDMP_CHECK(field && node && ptr && pid && w && amps, "inject: null array");
+  k_inject<<<(nnodes + 127) / 128, 128, 0, st>>>(field, node, ptr, nnodes, pid, w, amps, C, m);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+int interpolate(cudaStream_t st, const float* field, const int64_t* idx, const float* w,
+                int npts, int nc, float* out) {
+  if (npts <= 0) return SDMP_OK;
+  SDMP_CHECK(field && idx && w && out, "interpolate: null array");
+  k_interp<<<(npts + 127) / 128, 128, 0, st>>>(field, idx, w, npts, nc, out);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+// ---- parameter binding --------------------------------------------------
+
+__global__ void k_bind_scale(float* __restrict__ out, const float* __restrict__ in, int64_t n,
+                             float C) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = in[i];
+    out[i] = v != 0.f ? __fdiv_rn(C, v) : 0.f;
+  }
+}
+
+int bind_scale(cudaStream_t st, float* out, const float* in, int64_t n, float C) {
+  if (n <= 0) return SDMP_OK;
+  SDMP_CHECK(out && in, "bind_scale: null array");
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 8 * 148 * 8) blocks = 8 * 148 * 8;
+  k_bind_scale<<<(unsigned)blocks, 256, 0, st>>>(out, in, n, C);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+// ---- pack / unpack / box copy ---------------------------------------------
+
+struct BoxXfer {
+  const float* __restrict__ src;
+  float* __restrict__ dst;
+  int64_t ssx, ssy, dsx, dsy;  // strides (z stride 1)
+  int64_t soff, doff;          // element offset of the box origin
+  int ex, ey, ez;              // extent
+};
+
+// grid: x = z-chunks, y = y rows, z = x planes
+__global__ void k_box_copy(BoxXfer b) {
+  const int y = blockIdx.y, x = blockIdx.z;
+  const float* s = b.src + b.soff + x * b.ssx + y * b.ssy;
+  float* d = b.dst + b.doff + x * b.dsx + y * b.dsy;
+  for (int z = blockIdx.x * blockDim.x + threadIdx.x; z < b.ez; z += gridDim.x * blockDim.x)
+    d[z] = s[z];
+}
+
+static int box_copy_kernel(cudaStream_t st, const BoxXfer& b) {
+  if (b.ex <= 0 || b.ey <= 0 || b.ez <= 0) return SDMP_OK;
+  SDMP_CHECK(b.ey <= 65535 && b.ex <= 65535, "box copy extent too large");
+  int zb = (b.ez + 255) / 256;
+  if (zb > 8) zb = 8;
+  dim3 grid(zb, b.ey, b.ex);
+  k_box_copy<<<grid, 256, 0, st>>>(b);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+int pack(cudaStream_t st, const float* field, const int64_t full[3], const int64_t lo[3],
+         const int64_t hi[3], float* buf) {
+  Geom g;
+  int rc = make_geom(full, lo, hi, &g);
+  if (rc) return rc;
+  BoxXfer b{};
+  b.src = field; b.dst = buf;
+  b.ssx = g.sx; b.ssy = g.sy;
+  b.ex = g.hi[0] - g.lo[0]; b.ey = g.hi[1] - g.lo[1]; b.ez = g.hi[2] - g.lo[2];
+  b.dsy = b.ez; b.dsx = (int64_t)b.ey * b.ez;
+  b.soff = g.lo[0] * g.sx + g.lo[1] * g.sy + g.lo[2];
+  b.doff = 0;
+  return box_copy_kernel(st, b);
+}
+
+int unpack(cudaStream_t st, float* field, const int64_t full[3], const int64_t lo[3],
+           const int64_t hi[3], const float* buf) {
+  Geom g;
+  int rc = make_geom(full, lo, hi, &g);
+  if (rc) return rc;
+  BoxXfer b{};
+  b.src = buf; b.dst = field;
+  b.dsx = g.sx; b.dsy = g.sy;
+  b.ex = g.hi[0] - g.lo[0]; b.ey = g.hi[1] - g.lo[1]; b.ez = g.hi[2] - g.lo[2];
+  b.ssy = b.ez; b.ssx = (int64_t)b.ey * b.ez;
+  b.doff = g.lo[0] * g.sx + g.lo[1] * g.sy + g.lo[2];
+  b.soff = 0;
+  return box_copy_kernel(st, b);
+}
+
+int copy_box(cudaStream_t st, const float* src, const int64_t sfull[3], const int64_t slo[3],
+             float* dst, const int64_t dfull[3], const int64_t dlo[3], const int64_t ext[3],
+             int engine) {
+  for (int a = 0; a < 3; ++a) {
+    SDMP_CHECK(ext[a] >= 0, "negative extent");
+    SDMP_CHECK(slo[a] >= 0 && slo[a] + ext[a] <= sfull[a], "source box outside array");
+    SDMP_CHECK(dlo[a] >= 0 && dlo[a] + ext[a] <= dfull[a], "destination box outside array");
+  }
+  if (ext[0] == 0 || ext[1] == 0 || ext[2] == 0) return SDMP_OK;
+  if (engine == 0) {
+    cudaMemcpy3DParms p = {};
+    p.srcPtr = make_cudaPitchedPtr((void*)src, sfull[2] * sizeof(float), sfull[2], sfull[1]);
+    p.dstPtr = make_cudaPitchedPtr(dst, dfull[2] * sizeof(float), dfull[2], dfull[1]);
+    p.srcPos = make_cudaPos(slo[2] * sizeof(float), slo[1], slo[0]);
+    p.dstPos = make_cudaPos(dlo[2] * sizeof(float), dlo[1], dlo[0]);
+    p.extent = make_cudaExtent(ext[2] * sizeof(float), ext[1], ext[0]);
+    p.kind = cudaMemcpyDefault;
+    SDMP_CUDA(cudaMemcpy3DAsync(&p, st));
+    return SDMP_OK;
+  }
+  BoxXfer b{};
+  b.src = src; b.dst = dst;
+  b.ssy = sfull[2]; b.ssx = sfull[1] * sfull[2];
+  b.dsy = dfull[2]; b.dsx = dfull[1] * dfull[2];
+  b.soff = slo[0] * b.ssx + slo[1] * b.ssy + slo[2];
+  b.doff = dlo[0] * b.dsx + dlo[1] * b.dsy + dlo[2];
+  b.ex = (int)ext[0]; b.ey = (int)ext[1]; b.ez = (int)ext[2];
+  return box_copy_kernel(st, b);
+}
+
+// ---- completion flags ------------------------------------------------------
+
+struct FlagArgs {
+  uint32_t* ptr[32];
+  int n;
+  uint32_t value;
+  unsigned long long timeout_ns;
+  int* err;  // host-mapped watchdog word
+};
+
+// Writes `value` into each (peer) flag with system-scope release semantics,
+// after all prior work on the stream (copies into the peer's halo).
+__global__ void k_signal(FlagArgs a) {
+  const int i = threadIdx.x;
+  if (i >= a.n) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.ptr[i]), "r"(a.value) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spins (with backoff) until every flag >= value (wrap-safe), or the
+// watchdog expires: then records the failure and returns so the stream
+// never hangs (SPEC.md:468 watchdog).
+__global__ void k_wait(FlagArgs a) {
+  const int i = threadIdx.x;
+  if (i >= a.n) return;
+  const unsigned long long t0 = gtimer();
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.ptr[i]) : "memory");
+    if ((int32_t)(v - a.value) >= 0) break;
+    if (gtimer() - t0 > a.timeout_ns) {
+      atomicExch(a.err, 1);
+      break;
+    }
+    __nanosleep(200);
+  }
+}
+
+int signal_flags(cudaStream_t st, uint32_t* const* ptrs, int n, uint32_t value) {
+  if (n <= 0) return SDMP_OK;
+  SDMP_CHECK(n <= 32, "at most 32 flags per signal");
+  FlagArgs a{};
+  for (int i = 0; i < n; ++i) a.ptr[i] = ptrs[i];
+  a.n = n;
+  a.value = value;
+  k_signal<<<1, 32, 0, st>>>(a);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+int wait_flags(cudaStream_t st, uint32_t* const* ptrs, int n, uint32_t value,
+               unsigned long long timeout_ns, int* err) {
+  if (n <= 0) return SDMP_OK;
+  SDMP_CHECK(n <= 32, "at most 32 flags per wait");
+  FlagArgs a{};
+  for (int i = 0; i < n; ++i) a.ptr[i] = ptrs[i];
+  a.n = n;
+  a.value = value;
+  a.timeout_ns = timeout_ns;
+  a.err = err;
+  k_wait<<<1, 32, 0, st>>>(a);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+}  // namespace sdmp
+
+using namespace sdmp;
+
+extern "C" int sdmp_inject(void* stream, float* field, const int64_t* node, const int32_t* ptr,
+                           int32_t nnodes, const int32_t* pid, const float* w,
+                           const float* amps, float C, const float* m) {
+  return inject((cudaStream_t)stream, field, node, ptr, nnodes, pid, w, amps, C, m);
+}
+
+extern "C" int sdmp_interpolate(void* stream, const float* field, const int64_t* idx,
+                                const float* w, int32_t npts, int32_t ncorner, float* out) {
+  return interpolate((cudaStream_t)stream, field, idx, w, npts, ncorner, out);
+}
+
+extern "C" int sdmp_bind_scale(void* stream, float* out, const float* in, int64_t n, float C) {
+  return bind_scale((cudaStream_t)stream, out, in, n, C);
+}
+
+extern "C" int sdmp_pack(void* stream, const float* field, const int64_t full[3],
+                         const int64_t lo[3], const int64_t hi[3], float* buf) {
+  return pack((cudaStream_t)stream, field, full, lo, hi, buf);
+}
+
+extern "C" int sdmp_unpack(void* stream, float* field, const int64_t full[3],
+                           const int64_t lo[3], const int64_t hi[3], const float* buf) {
+  return unpack((cudaStream_t)stream, field, full, lo, hi, buf);
+}
+
+extern "C" int sdmp_copy_box(void* stream, const float* src, const int64_t src_full[3],
+                             const int64_t src_lo[3], float* dst, const int64_t dst_full[3],
+                             const int64_t dst_lo[3], const int64_t extent[3], int32_t engine) {
+  return copy_box((cudaStream_t)stream, src, src_full, src_lo, dst, dst_full, dst_lo, extent,
+                  engine);
+}

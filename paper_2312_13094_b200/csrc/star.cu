@@ -1,0 +1,502 @@
+// Star-stencil family (acoustic SO 4..16, diffusion) for sm_100a.
+//
+// Replaces SPEC.md:311 compute(box, equation) for acoustic_kernel
+// and diffusion_kernel.  The update is
+// the reference's solved equation (symbolics.py:629-674) in the algebraic
+// form u1 = A*u0 + B*u2 + S*L(u0), S = C/m or C, with the FD weights of
+// fd_coefficients (symbolics.py:468-487) bound to fp32 once.
+//
+// Two kernels share ONE per-point evaluation sequence (star_point) written
+// with explicit round-to-nearest intrinsics, so a point gets bit-identical
+// results whichever kernel computes it: multi-rank runs (CORE by the
+// streaming kernel, OWNED slabs by the generic one) equal single-rank runs
+// bit for bit.
+//
+//  * star_generic: one thread per point, taps through L1/L2.  Any radius,
+//    any alignment, 2D (radius_z = 0) included.  Used for thin OWNED slabs.
+//  * star_stream<R>: HBM-roofline kernel.  A CTA owns a 128(z) x 16(y) tile
+//    and streams along x (slowest axis).  Each thread keeps a float4 x-window
+//    of 2R+1 planes in registers; the centre plane (tile + R halo in y and z)
+//    is staged in shared memory for the y/z taps.  u0 is read from DRAM once
+//    (halo re-reads of neighbouring tiles hit L2), u2 and m are streamed
+//    once (evict-first), u1 written once: 16 B / point.
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace sdmp {
+
+struct StarParams {
+  const float* __restrict__ u0;
+  const float* __restrict__ u2;
+  const float* __restrict__ m;
+  float* __restrict__ u1;
+  Geom g;
+  int r[3];
+  float c[3][SDMP_NCOEF];
+  float csum0;  // c_x0 + c_y0 + c_z0 (fp32, host-rounded)
+  float A, B, C;
+  int m_is_scale;  // m holds the bound scale S = C/m (sdmp_bind_scale)
+};
+
+// Shared tail of the per-point update: u1 = A*u0 + B*u2 + S*lap.
+__device__ __forceinline__ float star_finish(const StarParams& p, float lap, float c0, float u2v,
+                                             float mv) {
+  float s = (p.m == nullptr) ? p.C : (p.m_is_scale ? mv : __fdiv_rn(p.C, mv));
+  float t = __fmul_rn(p.A, c0);
+  t = __fmaf_rn(p.B, u2v, t);
+  return __fmaf_rn(s, lap, t);
+}
+
+// Per-point update.  xs(k)/ys(k)/zs(k) return tap(-k) + tap(+k) along the
+// axis; the sum is formed with __fadd_rn inside the caller.
+template <int RX, int RY, int RZ, class FX, class FY, class FZ>
+__device__ __forceinline__ float star_point(const StarParams& p, float c0, float u2v, float mv,
+                                            int rx, int ry, int rz, FX xs, FY ys, FZ zs) {
+  float lap = __fmul_rn(p.csum0, c0);
+#pragma unroll
+  for (int k = 1; k <= (RX > 0 ? RX : SDMP_MAX_RADIUS); ++k)
+    if (RX > 0 || k <= rx) lap = __fmaf_rn(p.c[0][k], xs(k), lap);
+#pragma unroll
+  for (int k = 1; k <= (RY > 0 ? RY : SDMP_MAX_RADIUS); ++k)
+    if (RY > 0 || k <= ry) lap = __fmaf_rn(p.c[1][k], ys(k), lap);
+#pragma unroll
+  for (int k = 1; k <= (RZ > 0 ? RZ : SDMP_MAX_RADIUS); ++k)
+    if (RZ > 0 || k <= rz) lap = __fmaf_rn(p.c[2][k], zs(k), lap);
+  return star_finish(p, lap, c0, u2v, mv);
+}
+
+// ---------------------------------------------------------------------------
+// generic: one thread per point
+
+__global__ void __launch_bounds__(256) star_generic(StarParams p) {
+  const int z = p.g.lo[2] + blockIdx.x * 32 + threadIdx.x;
+  const int y = p.g.lo[1] + blockIdx.y * 8 + threadIdx.y;
+  const int x = p.g.lo[0] + blockIdx.z;
+  if (z >= p.g.hi[2] || y >= p.g.hi[1]) return;
+  const int64_t sx = p.g.sx, sy = p.g.sy;
+  const int64_t i = x * sx + y * sy + z;
+  const float* __restrict__ u = p.u0;
+  float c0 = __ldg(u + i);
+  float u2v = p.u2 ? __ldg(p.u2 + i) : 0.0f;
+  float mv = p.m ? __ldg(p.m + i) : 1.0f;
+  auto xs = [&](int k) { return __fadd_rn(__ldg(u + i - k * sx), __ldg(u + i + k * sx)); };
+  auto ys = [&](int k) { return __fadd_rn(__ldg(u + i - k * sy), __ldg(u + i + k * sy)); };
+  auto zs = [&](int k) { return __fadd_rn(__ldg(u + i - k), __ldg(u + i + k)); };
+  p.u1[i] = star_point<0, 0, 0>(p, c0, u2v, mv, p.r[0], p.r[1], p.r[2], xs, ys, zs);
+}
+
+// ---------------------------------------------------------------------------
+// streaming: register x-window + shared y/z plane
+
+constexpr int kTZ = 128;  // z points per tile (32 lanes x float4)
+constexpr int kTY = 16;   // y rows per tile (one warp per row)
+
+__host__ __device__ constexpr int round4(int r) { return (r + 3) & ~3; }
+
+template <int R>
+struct StreamSmem {
+  static constexpr int OFF = round4(R);           // left pad keeps float4 alignment
+  static constexpr int PITCH = OFF + kTZ + OFF;   // floats per smem row
+  static constexpr int ROWS = kTY + 2 * R;
+  static constexpr int BYTES = PITCH * ROWS * 4;
+};
+
+__device__ __forceinline__ float4 ld4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ float4 ld4_stream(const float* p) {
+  return __ldcs(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ float f4get(const float4& v, int j) {
+  return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+
+template <int R>
+__global__ void __launch_bounds__(kTZ / 4 * kTY, 1)
+star_stream(StarParams p, int xchunk) {
+  using S = StreamSmem<R>;
+  extern __shared__ __align__(16) float sm[];
+  const int tz = threadIdx.x, ty = threadIdx.y;
+  const int z0 = p.g.lo[2] + blockIdx.x * kTZ;
+  const int y0 = p.g.lo[1] + blockIdx.y * kTY;
+  const int xa = p.g.lo[0] + blockIdx.z * xchunk;
+  const int xb = min(xa + xchunk, p.g.hi[0]);
+  const int z = z0 + 4 * tz, y = y0 + ty;
+  const int64_t sx = p.g.sx, sy = p.g.sy;
+  // keep a window if this column feeds an active point's y/z taps
+  const bool feeds = (z < p.g.hi[2] + R) && (y < p.g.hi[1] + R);
+  const bool active = (z < p.g.hi[2]) && (y < p.g.hi[1]);
+  const float* __restrict__ u0 = p.u0;
+  const int64_t col = (int64_t)y * sy + z;
+
+  float4 w[2 * R + 1];
+  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < 2 * R; ++k)
+    w[k] = feeds ? ld4(u0 + (int64_t)(xa - R + k) * sx + col) : zero4;
+
+  // y-halo loaders: 2R rows x 32 float4
+  const int li = ty * 32 + tz;
+  const bool yh_load = li < 2 * R * 32;
+  const int yh_row = li / 32;                                  // 0..2R-1
+  const int yh_srow = yh_row < R ? yh_row : yh_row + kTY;      // smem row
+  const int yh_gy = y0 - R + yh_srow;
+  const int yh_z = z0 + 4 * (li % 32);
+  const bool yh_ok = yh_load && yh_gy < p.g.hi[1] + R && yh_z < p.g.hi[2] + R;
+  // z-halo loaders: kTY rows x 2R scalars
+  const bool zh_load = li < kTY * 2 * R;
+  const int zh_row = li / (2 * R);
+  const int zh_c = li % (2 * R);
+  const int zh_gz = zh_c < R ? z0 - R + zh_c : z0 + kTZ + (zh_c - R);
+  const int zh_scol = zh_c < R ? S::OFF - R + zh_c : S::OFF + kTZ + (zh_c - R);
+  const int zh_gy = y0 + zh_row;
+  const bool zh_ok = zh_load && zh_gy < p.g.hi[1] + R && zh_gz < p.g.hi[2] + R;
+
+  float* my_row = sm + (ty + R) * S::PITCH + S::OFF + 4 * tz;
+
+  for (int x = xa; x < xb; ++x) {
+    const int64_t px = (int64_t)x * sx;
+    if (feeds) w[2 * R] = ld4(u0 + px + R * sx + col);
+    float4 u2v = zero4, mv = make_float4(1.f, 1.f, 1.f, 1.f);
+    if (active) {
+      if (p.u2) u2v = ld4_stream(p.u2 + px + col);
+      if (p.m) mv = ld4_stream(p.m + px + col);
+    }
+    float4 yh = zero4;
+    if (yh_ok) yh = ld4(u0 + px + (int64_t)yh_gy * sy + yh_z);
+    float zh = 0.f;
+    if (zh_ok) zh = __ldg(u0 + px + (int64_t)zh_gy * sy + zh_gz);
+
+    *reinterpret_cast<float4*>(my_row) = w[R];
+    if (yh_load) *reinterpret_cast<float4*>(sm + yh_srow * S::PITCH + S::OFF + 4 * (li % 32)) = yh;
+    if (zh_load) sm[(zh_row + R) * S::PITCH + zh_scol] = zh;
+    __syncthreads();
+
+    if (active) {
+      // z window: positions z-OFF .. z+3+OFF as float4s
+      constexpr int NZW = (4 + 2 * S::OFF) / 4;
+      float zw[4 * NZW];
+#pragma unroll
+      for (int q = 0; q < NZW; ++q) {
+        float4 v = *reinterpret_cast<const float4*>(my_row - S::OFF + 4 * q);
+        zw[4 * q + 0] = v.x; zw[4 * q + 1] = v.y; zw[4 * q + 2] = v.z; zw[4 * q + 3] = v.w;
+      }
+      float4 yt_m[R], yt_p[R];
+#pragma unroll
+      for (int k = 1; k <= R; ++k) {
+        yt_m[k - 1] = *reinterpret_cast<const float4*>(my_row - k * S::PITCH);
+        yt_p[k - 1] = *reinterpret_cast<const float4*>(my_row + k * S::PITCH);
+      }
+      float out[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        auto xs = [&](int k) { return __fadd_rn(f4get(w[R - k], j), f4get(w[R + k], j)); };
+        auto ys = [&](int k) { return __fadd_rn(f4get(yt_m[k - 1], j), f4get(yt_p[k - 1], j)); };
+        auto zs = [&](int k) { return __fadd_rn(zw[S::OFF + j - k], zw[S::OFF + j + k]); };
+        out[j] = star_point<R, R, R>(p, f4get(w[R], j), f4get(u2v, j), f4get(mv, j),
+                                     R, R, R, xs, ys, zs);
+      }
+      __stcs(reinterpret_cast<float4*>(p.u1 + px + col),
+             make_float4(out[0], out[1], out[2], out[3]));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2 * R; ++k) w[k] = w[k + 1];
+  }
+}
+
+template <int R>
+static int launch_stream(const StarParams& p, cudaStream_t st) {
+  using S = StreamSmem<R>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SDMP_CUDA(cudaFuncSetAttribute(star_stream<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   S::BYTES));
+    attr_set = true;
+  }
+  const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
+  dim3 block(kTZ / 4, kTY);
+  const int tz = (nz + kTZ - 1) / kTZ, ty = (ny + kTY - 1) / kTY;
+  // ~4 CTAs per SM in total, but keep x chunks >= 8R planes so the
+  // window priming (2R planes) stays a small overhead.
+  const int64_t tiles = (int64_t)tz * ty;
+  int64_t want = (4ll * num_sms() + tiles - 1) / tiles;
+  int64_t maxchunks = nx / (8 * R) > 0 ? nx / (8 * R) : 1;
+  int nch = (int)(want < maxchunks ? want : maxchunks);
+  if (nch < 1) nch = 1;
+  if (nch > 65535) nch = 65535;
+  const int chunk = (nx + nch - 1) / nch;
+  nch = (nx + chunk - 1) / chunk;
+  dim3 grid(tz, ty, nch);
+  star_stream<R><<<grid, block, S::BYTES, st>>>(p, chunk);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// TMA pipeline: one producer warp streams plane tiles into an S-stage shared
+// ring with cp.async.bulk.tensor (mbarrier complete_tx); TY consumer warps
+// (one y row each, float4 along z) keep the x-window in registers and read
+// y/z taps from the staged centre plane.  No __syncthreads in the loop.
+//
+// Per pipeline iteration i (plane p = xa - R + i):
+//   front  [TY][128]            u0 at plane p         -> register window
+//   centre [TY+2R][128+2*OFF]   u0 at plane p-R (=x)  -> y/z taps   (i >= 2R)
+//   u2, m  [TY][128]            at plane x                          (i >= 2R)
+
+template <int R, int TY>
+struct TmaCfg {
+  static constexpr int OFF = round4(R);
+  static constexpr int CZ = kTZ + 2 * OFF;
+  static constexpr int CY = TY + 2 * R;
+  static constexpr int FRONT = kTZ * TY * 4;
+  static constexpr int CENTER = ((CZ * CY * 4) + 127) & ~127;
+  static constexpr int STAGE = 3 * FRONT + CENTER;
+  static constexpr int S = 4;
+  static constexpr int BYTES = S * STAGE + 2 * S * 8 + 128;
+  static constexpr int THREADS = 32 * (TY + 1);
+};
+
+template <int R, int TY>
+__global__ void __launch_bounds__(TmaCfg<R, TY>::THREADS, 1)
+star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ CUtensorMap tm_center,
+         const __grid_constant__ CUtensorMap tm_u2, const __grid_constant__ CUtensorMap tm_m,
+         StarParams p, int xchunk) {
+  using T = TmaCfg<R, TY>;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sm + T::S * T::STAGE);
+  uint64_t* empty_bar = full_bar + T::S;
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const bool has_u2 = p.u2 != nullptr, has_m = p.m != nullptr;
+  if (lane == 0 && warp == 0) {
+    for (int s = 0; s < T::S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], TY);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int z0 = p.g.lo[2] + blockIdx.x * kTZ;
+  const int y0 = p.g.lo[1] + blockIdx.y * TY;
+  const int xa = p.g.lo[0] + blockIdx.z * xchunk;
+  const int xb = min(xa + xchunk, p.g.hi[0]);
+  const int nit = (xb - xa) + 2 * R;
+
+  if (warp == TY) {  // producer
+    if (lane == 0) {
+      prefetch_tmap(&tm_front);
+      prefetch_tmap(&tm_center);
+      const uint32_t main_bytes =
+          T::FRONT + T::CZ * T::CY * 4 + (has_u2 ? T::FRONT : 0) + (has_m ? T::FRONT : 0);
+      for (int i = 0; i < nit; ++i) {
+        const int s = i % T::S;
+        mbar_wait(&empty_bar[s], ((i / T::S) & 1) ^ 1);
+        unsigned char* st = sm + s * T::STAGE;
+        const bool main = i >= 2 * R;
+        mbar_arrive_expect_tx(&full_bar[s], main ? main_bytes : (uint32_t)T::FRONT);
+        tma_load_3d(st, &tm_front, &full_bar[s], z0, y0, xa - R + i);
+        if (main) {
+          const int x = xa + i - 2 * R;
+          tma_load_3d(st + T::FRONT, &tm_center, &full_bar[s], z0 - T::OFF, y0 - R, x);
+          if (has_u2) tma_load_3d(st + T::FRONT + T::CENTER, &tm_u2, &full_bar[s], z0, y0, x);
+          if (has_m)
+            tma_load_3d(st + 2 * T::FRONT + T::CENTER, &tm_m, &full_bar[s], z0, y0, x);
+        }
+      }
+    }
+    return;
+  }
+
+  const int z = z0 + 4 * lane, y = y0 + warp;
+  const bool active = (z < p.g.hi[2]) && (y < p.g.hi[1]);
+  const int64_t sx = p.g.sx, sy = p.g.sy;
+  const int64_t col = (int64_t)y * sy + z;
+  float4 w[2 * R + 1];
+#pragma unroll
+  for (int k = 0; k <= 2 * R; ++k) w[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  for (int i = 0; i < nit; ++i) {
+    const int s = i % T::S;
+    mbar_wait(&full_bar[s], (i / T::S) & 1);
+    const unsigned char* st = sm + s * T::STAGE;
+#pragma unroll
+    for (int k = 0; k < 2 * R; ++k) w[k] = w[k + 1];
+    w[2 * R] = *reinterpret_cast<const float4*>(
+        reinterpret_cast<const float*>(st) + warp * kTZ + 4 * lane);
+    if (i >= 2 * R && active) {
+      const int x = xa + i - 2 * R;
+      const float* row = reinterpret_cast<const float*>(st + T::FRONT) + (warp + R) * T::CZ +
+                         T::OFF + 4 * lane;
+      constexpr int NZW = (4 + 2 * T::OFF) / 4;
+      float zw[4 * NZW];
+#pragma unroll
+      for (int q = 0; q < NZW; ++q) {
+        float4 v = *reinterpret_cast<const float4*>(row - T::OFF + 4 * q);
+        zw[4 * q + 0] = v.x; zw[4 * q + 1] = v.y; zw[4 * q + 2] = v.z; zw[4 * q + 3] = v.w;
+      }
+      float4 u2v = make_float4(0.f, 0.f, 0.f, 0.f), mv = make_float4(1.f, 1.f, 1.f, 1.f);
+      if (has_u2)
+        u2v = *reinterpret_cast<const float4*>(
+            reinterpret_cast<const float*>(st + T::FRONT + T::CENTER) + warp * kTZ + 4 * lane);
+      if (has_m)
+        mv = *reinterpret_cast<const float4*>(
+            reinterpret_cast<const float*>(st + 2 * T::FRONT + T::CENTER) + warp * kTZ + 4 * lane);
+      // same operation order per point as star_point (x, y, z taps; k
+      // ascending), vectorised over the 4 z points of this thread
+      float lap[4], out[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) lap[j] = __fmul_rn(p.csum0, f4get(w[R], j));
+#pragma unroll
+      for (int k = 1; k <= R; ++k)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          lap[j] = __fmaf_rn(p.c[0][k], __fadd_rn(f4get(w[R - k], j), f4get(w[R + k], j)), lap[j]);
+#pragma unroll
+      for (int k = 1; k <= R; ++k) {
+        const float4 a = *reinterpret_cast<const float4*>(row - k * T::CZ);
+        const float4 b = *reinterpret_cast<const float4*>(row + k * T::CZ);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          lap[j] = __fmaf_rn(p.c[1][k], __fadd_rn(f4get(a, j), f4get(b, j)), lap[j]);
+      }
+#pragma unroll
+      for (int k = 1; k <= R; ++k)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          lap[j] = __fmaf_rn(p.c[2][k], __fadd_rn(zw[T::OFF + j - k], zw[T::OFF + j + k]), lap[j]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        out[j] = star_finish(p, lap[j], f4get(w[R], j), f4get(u2v, j), f4get(mv, j));
+      __stcs(reinterpret_cast<float4*>(p.u1 + (int64_t)x * sx + col),
+             make_float4(out[0], out[1], out[2], out[3]));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
+  }
+}
+
+// Pick the number of x chunks: whole waves of one CTA per SM, small
+// priming overhead (2R front-only iterations per chunk).
+static int pick_chunks(int64_t tiles, int nx, int R, int ctas_per_sm) {
+  const int64_t slots = (int64_t)num_sms() * ctas_per_sm;
+  double best = 1e30;
+  int best_n = 1;
+  for (int n = 1; n <= 64 && n <= nx; ++n) {
+    const int chunk = (nx + n - 1) / n;
+    const int64_t items = tiles * ((nx + chunk - 1) / chunk);
+    const int64_t waves = (items + slots - 1) / slots;
+    const double cost = (double)waves * (chunk + 0.35 * 2 * R);
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_n = n;
+    }
+  }
+  return best_n;
+}
+
+template <int R, int TY>
+static int launch_tma(const StarParams& p, cudaStream_t st, const int64_t full[3]) {
+  using T = TmaCfg<R, TY>;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    SDMP_CUDA(cudaFuncSetAttribute(star_tma<R, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   T::BYTES));
+    attr_dev = dev;
+  }
+  CUtensorMap tf, tc, t2, tm;
+  int rc = make_tmap_3d(&tf, p.u0, full, kTZ, TY, false);
+  if (!rc) rc = make_tmap_3d(&tc, p.u0, full, T::CZ, T::CY, false);
+  if (!rc) rc = make_tmap_3d(&t2, p.u2 ? p.u2 : p.u0, full, kTZ, TY, true);
+  if (!rc) rc = make_tmap_3d(&tm, p.m ? p.m : p.u0, full, kTZ, TY, true);
+  if (rc) return rc;
+  const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
+  const int tz = (nz + kTZ - 1) / kTZ, ty = (ny + TY - 1) / TY;
+  int nch = pick_chunks((int64_t)tz * ty, nx, R, 1);
+  const int chunk = (nx + nch - 1) / nch;
+  nch = (nx + chunk - 1) / chunk;
+  SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");
+  dim3 grid(tz, ty, nch), block(32, TY + 1);
+  star_tma<R, TY><<<grid, block, T::BYTES, st>>>(tf, tc, t2, tm, p, chunk);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+static int launch_generic(const StarParams& p, cudaStream_t st) {
+  const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
+  SDMP_CHECK(nx <= 65535, "generic kernel: box x extent > 65535");
+  dim3 block(32, 8);
+  dim3 grid((nz + 31) / 32, (ny + 7) / 8, nx);
+  star_generic<<<grid, block, 0, st>>>(p);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+int star_update(cudaStream_t st, const float* u0, const float* u2, const float* m, float* u1,
+                const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
+                const int32_t radius[3], const float* coeffs, float A, float B, float C,
+                int variant) {
+  StarParams p;
+  int rc = make_geom(full, lo, hi, &p.g);
+  if (rc) return rc;
+  SDMP_CHECK(u0 && u1, "u0/u1 must be non-null");
+  SDMP_CHECK(B == 0.0f || u2, "u2 required when B != 0");
+  if (box_empty(p.g)) return SDMP_OK;
+  p.u0 = u0; p.u2 = (B == 0.0f) ? nullptr : u2; p.m = m; p.u1 = u1;
+  p.m_is_scale = (variant & SDMP_VARIANT_M_IS_SCALE) ? 1 : 0;
+  variant &= 0xff;
+  float cs = 0.f;
+  for (int a = 0; a < 3; ++a) {
+    SDMP_CHECK(radius[a] >= 0 && radius[a] <= SDMP_MAX_RADIUS, "radius outside 0..8");
+    SDMP_CHECK(lo[a] >= radius[a] && hi[a] + radius[a] <= full[a], "box + radius exceeds FULL");
+    p.r[a] = radius[a];
+    for (int k = 0; k < SDMP_NCOEF; ++k) p.c[a][k] = (k <= radius[a]) ? coeffs[a * SDMP_NCOEF + k] : 0.f;
+    cs = cs + p.c[a][0];  // (cx0 + cy0) + cz0
+  }
+  p.csum0 = cs;
+  p.A = A; p.B = B; p.C = C;
+
+  const int R = radius[0];
+  const bool streamable = radius[1] == R && radius[2] == R && R >= 1 &&
+                          (full[2] % 4 == 0) && (lo[2] % 4 == 0) && ((hi[2] - lo[2]) % 4 == 0) &&
+                          (((uintptr_t)u0 | (uintptr_t)u1 | (uintptr_t)u2 | (uintptr_t)m) % 16 == 0);
+  // unaligned / unequal-radius boxes always take the generic kernel
+  if (variant == 1 || !streamable) return launch_generic(p, st);
+  if (variant == 2) {
+    switch (R) {
+      case 1: return launch_stream<1>(p, st);
+      case 2: return launch_stream<2>(p, st);
+      case 3: return launch_stream<3>(p, st);
+      case 4: return launch_stream<4>(p, st);
+      case 5: return launch_stream<5>(p, st);
+      case 6: return launch_stream<6>(p, st);
+      case 7: return launch_stream<7>(p, st);
+      case 8: return launch_stream<8>(p, st);
+    }
+  }
+  switch (R) {  // variant 0 (auto) / 3: TMA pipeline
+    case 1: return launch_tma<1, 16>(p, st, full);
+    case 2: return launch_tma<2, 16>(p, st, full);
+    case 3: return launch_tma<3, 16>(p, st, full);
+    case 4: return launch_tma<4, 16>(p, st, full);
+    case 5: return launch_tma<5, 16>(p, st, full);
+    case 6: return launch_tma<6, 8>(p, st, full);
+    case 7: return launch_tma<7, 8>(p, st, full);
+    case 8: return launch_tma<8, 8>(p, st, full);
+  }
+  return launch_generic(p, st);
+}
+
+}  // namespace sdmp
+
+extern "C" int sdmp_star_update(void* stream, const float* u0, const float* u2, const float* m,
+                                float* u1, const int64_t full[3], const int64_t lo[3],
+                                const int64_t hi[3], const int32_t radius[3],
+                                const float* coeffs, float A, float B, float C,
+                                int32_t variant) {
+  return sdmp::star_update((cudaStream_t)stream, u0, u2, m, u1, full, lo, hi, radius, coeffs,
+                           A, B, C, variant);
+}
