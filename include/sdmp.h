@@ -168,9 +168,10 @@ int sdmp_plan_add_action(sdmp_plan* plan, const int64_t* ints, int32_t nints,
 int sdmp_plan_run(sdmp_plan* plan, int64_t time_m, int64_t time_M, void* stream);
 /* Block until the plan's streams drain; checks the halo watchdog. */
 int sdmp_plan_sync(sdmp_plan* plan);
-/* Per-action instrumentation: enable (records events around each action of
- * the next run) and read {action index, stream, kind, start_ms, end_ms}
- * rows relative to the run start for the last step. */
+/* Per-action instrumentation: enable (records CUDA events around every
+ * action of every step, on the action's stream) and read 6 doubles per
+ * action {index, stream, kind, mean start ms from the step start, mean
+ * duration ms, kernel launches per step} averaged over the last run. */
 int sdmp_plan_set_tracing(sdmp_plan* plan, int32_t on);
 int sdmp_plan_trace(sdmp_plan* plan, double* rows, int32_t max_rows, int32_t* nrows);
 /* Watchdog for halo waits in milliseconds (default 30000). */

@@ -1,0 +1,499 @@
+"""Operator compiler: kernel-family recognition, HaloSpot detection and
+optimisation, and lowering of the three exchange modes to an ExecPlan.
+
+Implements the SPEC's ``compiler`` module for the B200
+path:
+
+* ``recognise`` — each solved update (``StencilEquation``) is matched
+  EXACTLY against a kernel-family template by rational probing (the
+  ``rational_probe`` idea of test_symbolics.py:152-164): the rhs is linear in
+  the field accesses, so its coefficients are extracted with ``eval_exact``
+  at random rational bindings and checked against the family's algebraic
+  form.  Unrecognised equations raise — there is no generic/CPU fallback.
+* ``halo_phases`` — per-kernel read radii (``build_clusters``,
+  SPEC.md:328-336), HaloSpots placed before the first dependent kernel and
+  optimised: drop (field not dirty), merge (adjacent spots), hoist
+  (read-only coefficient fields exchanged once before the time loop)
+  (``optimize_halospots``).
+* ``ExecPlan`` — ``lower_mode``: basic = axis-sequenced
+  face exchange then DOMAIN; diagonal = single-step exchange then DOMAIN;
+  full = post, CORE, wait, OWNED slabs (Listing 8).  The same ExecPlan is
+  instantiated per rank into native actions (``runtime_plan.py``).
+"""
+from __future__ import annotations
+
+import random
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from . import symbolics as S
+
+MODES = ("basic", "diagonal", "full")
+_MODE_ALIASES = {"1": "basic", "basic": "basic", "diag": "diagonal", "diag2": "diagonal",
+                 "diagonal": "diagonal", "full": "full", "overlap": "full"}
+
+
+class CompilerError(S.SymbolicsError):
+    """Equation not recognised / plan cannot be built."""
+
+
+def normalise_mode(mode) -> str:
+    m = _MODE_ALIASES.get(str(mode).lower())
+    if m is None:
+        raise CompilerError(f"unknown mpi mode {mode!r}; expected basic | diagonal | full")
+    return m
+
+
+# ---------------------------------------------------------------------------
+# Kernel families
+
+
+@dataclass
+class StarKernel:
+    """u1 = A u0 + B u2 + S L(u0),  S = c * dt^p * m^q  (q in {0, -1}).
+
+    Acoustic: (A, B, c, p, q) = (2, -1, 1, 2, -1) — the reference's solved
+    ``m*u.dt2 - u.laplace`` (symbolics.py:629-674); diffusion: (1, 0, 1, 1, 0)
+    — ``Eq(u.dt, u.laplace)``."""
+
+    u: S.FieldSpec
+    m: Optional[S.FieldSpec]
+    A: Fraction
+    B: Fraction
+    c: Fraction
+    p: int
+    q: int
+    weights: Tuple[Tuple[Fraction, ...], ...]  # per axis, centre-out w_k (k = 0..r)
+    family: str = "star"
+
+    @property
+    def radius(self) -> Tuple[int, ...]:
+        return tuple(len(w) - 1 for w in self.weights)
+
+    def reads(self):
+        """(field, tshift, radius per axis) read by the kernel."""
+        out = [(self.u, 0, self.radius)]
+        if self.B != 0:
+            out.append((self.u, -1, (0,) * len(self.radius)))
+        if self.m is not None:
+            out.append((self.m, 0, (0,) * len(self.radius)))
+        return out
+
+    def writes(self):
+        return [(self.u, 1)]
+
+    @property
+    def bytes_per_point(self) -> int:
+        """Algorithmic HBM bytes per updated point (each array once)."""
+        return 4 * (2 + (1 if self.B != 0 else 0) + (1 if self.m is not None else 0))
+
+
+@dataclass
+class TTIKernel:
+    """Two-field pseudo-acoustic TTI."""
+
+    p: S.FieldSpec
+    r: S.FieldSpec
+    m: S.FieldSpec
+    epsp: S.FieldSpec
+    delp: S.FieldSpec
+    a: Tuple[S.FieldSpec, S.FieldSpec, S.FieldSpec]
+    so: int
+    family: str = "tti"
+
+    @property
+    def radius(self):
+        return (self.so // 2,) * 3
+
+    def reads(self):
+        nest = (self.so,) * 3
+        zero = (0, 0, 0)
+        out = [(self.p, 0, nest), (self.r, 0, nest), (self.p, -1, zero), (self.r, -1, zero),
+               (self.m, 0, zero), (self.epsp, 0, zero), (self.delp, 0, zero)]
+        out += [(ai, 0, self.radius) for ai in self.a]
+        return out
+
+    def writes(self):
+        return [(self.p, 1), (self.r, 1)]
+
+    bytes_per_point = 48
+
+
+@dataclass
+class StaggeredPhase:
+    """One phase of the staggered elastic / viscoelastic system."""
+
+    kind: str  # "v" | "t" | "visco_t"
+    v: Tuple[S.FieldSpec, ...]
+    tau: Tuple[S.FieldSpec, ...]
+    params: Tuple[S.FieldSpec, ...]  # (b,) | (lam, mu) | (l2m, mus, its)
+    mem: Tuple[S.FieldSpec, ...] = ()
+    so: int = 8
+    family: str = "staggered"
+
+    @property
+    def radius(self):
+        return (self.so // 2,) * 3
+
+    def reads(self):
+        r, zero = self.radius, (0, 0, 0)
+        if self.kind == "v":
+            return ([(f, 0, r) for f in self.tau] + [(f, 0, zero) for f in self.v]
+                    + [(self.params[0], 0, zero)])
+        out = [(f, 1, r) for f in self.v] + [(f, 0, zero) for f in self.tau]
+        out += [(f, 0, zero) for f in self.mem] + [(f, 0, zero) for f in self.params]
+        return out
+
+    def writes(self):
+        if self.kind == "v":
+            return [(f, 1) for f in self.v]
+        return [(f, 1) for f in self.tau] + [(f, 1) for f in self.mem]
+
+    @property
+    def bytes_per_point(self) -> int:
+        if self.kind == "v":
+            return 4 * 13
+        if self.kind == "t":
+            return 4 * 17
+        return 4 * 30
+
+
+# ---------------------------------------------------------------------------
+# Recognition by exact rational probing
+
+
+def _leaves(e: S.Expr):
+    return {n for n in S.walk(e) if isinstance(n, (S.Symbol, S.FieldAccess))}
+
+
+def _coefficients(rhs: S.Expr, unknowns: List[S.FieldAccess], binding: dict) -> dict:
+    """Coefficient of each unknown access in a rhs that is linear in them."""
+    base = dict(binding)
+    for acc in unknowns:
+        base[acc] = Fraction(0)
+    c0 = S.eval_exact(rhs, base)
+    out = {}
+    for acc in unknowns:
+        b = dict(base)
+        b[acc] = Fraction(1)
+        out[acc] = S.eval_exact(rhs, b) - c0
+    # linearity / no affine constant: check on a random point as well
+    rng = random.Random(7)
+    b = dict(binding)
+    vals = {acc: Fraction(rng.randint(-9, 9), rng.randint(1, 7)) for acc in unknowns}
+    b.update(vals)
+    if S.eval_exact(rhs, b) != c0 + sum(out[a] * vals[a] for a in unknowns) or c0 != 0:
+        raise CompilerError("update is not linear-homogeneous in the field accesses")
+    return out
+
+
+def recognise_star(eq: S.StencilEquation) -> Optional[StarKernel]:
+    """Match ``u1 = A u0 + B u2 + c dt^p m^q L(u0)`` exactly (or None)."""
+    u = eq.lhs.spec
+    if u.is_static or eq.lhs.tshift != 1 or any(eq.lhs.offsets):
+        return None
+    accs = S.accesses(eq.rhs) + [a for _, t in eq.temporaries for a in S.accesses(t)]
+    if eq.temporaries:
+        return None  # solve_forward output has none; CSE'd forms are re-solved upstream
+    evolving = {a for a in accs if a.spec == u}
+    statics = {a.spec for a in accs if a.spec != u}
+    if any(a.spec != u and (not a.spec.is_static or any(a.offsets)) for a in accs):
+        return None
+    if len(statics) > 1:
+        return None
+    m = next(iter(statics)) if statics else None
+    nd = u.grid.ndims
+    if any(a.tshift not in (0, -1) for a in evolving):
+        return None
+    if any(a.tshift == -1 and any(a.offsets) for a in evolving):
+        return None
+    r = u.space_order // 2
+    weights = [Fraction(w) for w in S.fd_coefficients(2, u.space_order)]
+    W = tuple(weights[r + k] for k in range(r + 1))
+    # expected access set: u0 star of radius r, u2 (optional), m[0]
+    star = {S.FieldAccess(u, 0, tuple(k if b == a else 0 for b in range(nd)))
+            for a in range(nd) for k in range(-r, r + 1)}
+    u0s = {a for a in evolving if a.tshift == 0}
+    if not u0s <= star:
+        return None
+    unknowns = sorted(u0s | {a for a in evolving if a.tshift == -1},
+                      key=lambda a: (a.tshift, a.offsets))
+    rng = random.Random(1234)
+    samples = []
+    for _ in range(3):
+        bind = {}
+        dt = Fraction(rng.randint(2, 30), rng.randint(2, 30))
+        hs = [Fraction(rng.randint(2, 40), rng.randint(1, 9)) for _ in range(nd)]
+        mv = Fraction(rng.randint(2, 50), rng.randint(2, 17))
+        for leaf in _leaves(eq.rhs):
+            if isinstance(leaf, S.Symbol):
+                if leaf.name == "dt":
+                    bind[leaf] = dt
+                elif leaf.name.startswith("h_"):
+                    bind[leaf] = hs[S.AXIS_NAMES.index(leaf.name[2:])]
+                else:
+                    return None
+            elif leaf.spec == m:
+                bind[leaf] = mv
+        coeffs = _coefficients(eq.rhs, unknowns, bind)
+        samples.append((dt, hs, mv, coeffs))
+    k1 = S.FieldAccess(u, 0, tuple(1 if b == 0 else 0 for b in range(nd)))
+    if W[1] == 0:
+        return None
+    centre = S.FieldAccess(u, 0, (0,) * nd)
+    prev = S.FieldAccess(u, -1, (0,) * nd)
+    scales, AB = [], set()
+    for dt, hs, mv, co in samples:
+        Sv = co.get(k1, Fraction(0)) * hs[0] ** 2 / W[1]
+        if Sv == 0:
+            return None
+        for a in range(nd):
+            for k in range(1, r + 1):
+                for sgn in (-1, 1):
+                    acc = S.FieldAccess(u, 0, tuple(sgn * k if b == a else 0 for b in range(nd)))
+                    if co.get(acc, Fraction(0)) != Sv * W[k] / hs[a] ** 2:
+                        return None
+        A = co.get(centre, Fraction(0)) - Sv * sum(W[0] / h ** 2 for h in hs)
+        AB.add((A, co.get(prev, Fraction(0))))
+        scales.append((dt, mv, Sv))
+    if len(AB) != 1:
+        return None
+    A0, B0 = AB.pop()
+    # S = c * dt^p * m^q: exactly one (p, q) gives a sample-independent c
+    cands = [(p, q) for p in (0, 1, 2) for q in ((0, -1) if m is not None else (0,))]
+    fits = [(p, q) for p, q in cands
+            if len({Sv / (dt ** p * mv ** q) for dt, mv, Sv in scales}) == 1]
+    if len(fits) != 1:
+        return None
+    pq = fits[0]
+    dt, mv, Sv = scales[0]
+    c0 = Sv / (dt ** pq[0] * mv ** pq[1])
+    if B0 != 0 and u.time_order < 2:
+        return None
+    if pq[1] == 0:
+        m = None
+    return StarKernel(u=u, m=m, A=A0, B=B0, c=c0, p=pq[0], q=pq[1],
+                      weights=tuple(W for _ in range(nd)))
+
+
+# Registry of family equations built by paper_2312_13094_b200.kernels; the
+# Operator matches user equations against it by structural equality.
+_FAMILY_REGISTRY: Dict[S.StencilEquation, object] = {}
+
+
+def register_family(eq: S.StencilEquation, kernel) -> None:
+    _FAMILY_REGISTRY[eq] = kernel
+
+
+def recognise(equations: Sequence) -> List[object]:
+    """Solved updates -> kernel list (one kernel may own several updates)."""
+    kernels: List[object] = []
+    seen = set()
+    for eq in equations:
+        if isinstance(eq, (StarKernel, TTIKernel, StaggeredPhase)):
+            kernels.append(eq)
+            continue
+        if not isinstance(eq, S.StencilEquation):
+            raise CompilerError(f"expected a solved update, got {type(eq).__name__}")
+        fam = _FAMILY_REGISTRY.get(eq)
+        if fam is not None:
+            if id(fam) not in seen:
+                seen.add(id(fam))
+                kernels.append(fam)
+            continue
+        k = recognise_star(eq)
+        if k is None:
+            raise CompilerError(
+                "equation not recognised as a supported kernel family (acoustic, "
+                "diffusion, TTI, staggered elastic/viscoelastic): "
+                + " ; ".join(S.format_equation(eq))[:300])
+        kernels.append(k)
+    return kernels
+
+
+# ---------------------------------------------------------------------------
+# HaloSpots
+
+
+@dataclass
+class HaloSpot:
+    """Exchange of ``fields`` (spec, tshift) with per-axis ``radius``."""
+
+    fields: List[Tuple[S.FieldSpec, int]]
+    radius: Tuple[int, ...]
+
+
+@dataclass
+class Phase:
+    halo: Optional[HaloSpot]
+    kernel: object
+
+
+@dataclass
+class HaloAnalysis:
+    hoisted: Optional[HaloSpot]
+    phases: List[Phase]
+    exchanges_per_step: int
+
+
+def halo_phases(kernels: Sequence, nranks: int) -> HaloAnalysis:
+    """build_clusters + optimize_halospots."""
+    nd = None
+    written = set()
+    for k in kernels:
+        for f, _t in k.writes():
+            written.add(f)
+    # static fields read with offsets -> hoisted once before the loop
+    hoist_fields, hoist_r = [], None
+    # dirty buffers at step start: everything written last step (tshift 0
+    # relative to the new step is the old tshift +1)
+    dirty = {(f, 0) for f in written}
+    phases = []
+    count = 0
+    for k in kernels:
+        need, rad = [], None
+        for f, t, r in k.reads():
+            nd = len(r)
+            if not any(r) or nranks == 1:
+                continue
+            if f.is_static:
+                if (f, 0) not in hoist_fields:
+                    hoist_fields.append((f, 0))
+                hoist_r = tuple(max(a, b) for a, b in zip(hoist_r or r, r))
+                continue
+            if (f, t) in dirty:
+                if (f, t) not in [x[0:2] for x in need]:
+                    need.append((f, t))
+                rad = tuple(max(a, b) for a, b in zip(rad or r, r))
+        spot = None
+        if need:
+            spot = HaloSpot(need, rad)
+            count += 1
+            for ft in need:
+                dirty.discard(ft)
+        phases.append(Phase(spot, k))
+        for f, t in k.writes():
+            dirty.add((f, t))
+    hoisted = HaloSpot(hoist_fields, hoist_r) if hoist_fields else None
+    return HaloAnalysis(hoisted, phases, count)
+
+
+# ---------------------------------------------------------------------------
+# ExecPlan (per-rank action list in terms of boxes; lowered to native ids by
+# runtime_plan.py)
+
+
+@dataclass
+class Action:
+    kind: str                 # post | wait | compute | inject | interp | record | streamwait
+    stream: int
+    phase: int = -1           # epoch phase index (post / wait)
+    spot: Optional[HaloSpot] = None
+    messages: list = field(default_factory=list)
+    kernel: object = None
+    box: tuple = None         # DOMAIN coordinates
+    region: str = ""
+    event: int = -1
+    sparse: object = None
+
+
+@dataclass
+class ExecPlan:
+    mode: str
+    actions: List[Action]
+    phases_per_step: int
+    hoisted: Optional[HaloSpot]
+    hoisted_messages: list
+
+    def kinds(self) -> List[str]:
+        return [a.kind if a.kind != "compute" else f"compute:{a.region}" for a in self.actions]
+
+    def message_count(self) -> int:
+        return sum(len(a.messages) for a in self.actions if a.kind == "post")
+
+
+def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
+               sparse_terms: Sequence = ()) -> ExecPlan:
+    """Per-rank ExecPlan for ``mode``."""
+    from .distfield import (RegionName, basic_messages, diagonal_messages,
+                            rank_regions)
+
+    mode = normalise_mode(mode)
+    nd = decomp.ndims
+    acts: List[Action] = []
+    epoch = 0
+    ev = 0
+    shape = decomp.local_shape(rank)
+    domain = ((0,) * nd, tuple(shape))
+    interps = [t for t in sparse_terms if t.kind == "interp"]
+    injects = [t for t in sparse_terms if t.kind == "inject"]
+
+    def kernel_reads_field(k, spec):
+        return any(f == spec for f, _t, _r in k.reads())
+
+    def kernel_writes_field(k, spec):
+        return any(f == spec for f, _t in k.writes())
+
+    for pi, ph in enumerate(analysis.phases):
+        k = ph.kernel
+        spot = ph.halo
+        my_interps = [t for t in interps if kernel_reads_field(k, t.field)
+                      and t not in [a.sparse for a in acts if a.kind == "interp"]]
+        my_injects = [t for t in injects if kernel_writes_field(k, t.field)]
+        if spot is not None:
+            # the exchange stream must see this step's previous compute
+            acts.append(Action("record", 0, event=ev))
+            acts.append(Action("streamwait", 2, event=ev))
+            ev += 1
+        if spot is None:
+            for t in my_interps:
+                acts.append(Action("interp", 0, sparse=t))
+            acts.append(Action("compute", 0, kernel=k, box=domain, region="DOMAIN"))
+        elif mode == "basic":
+            steps = basic_messages(decomp, rank, spot.radius)
+            for a in range(nd):
+                acts.append(Action("post", 2, phase=epoch, spot=spot, messages=steps[a]))
+                acts.append(Action("wait", 2, phase=epoch, spot=spot, messages=steps[a]))
+                epoch += 1
+            acts.append(Action("record", 2, event=ev))
+            acts.append(Action("streamwait", 0, event=ev))
+            ev += 1
+            for t in my_interps:
+                acts.append(Action("interp", 0, sparse=t))
+            acts.append(Action("compute", 0, kernel=k, box=domain, region="DOMAIN"))
+        elif mode == "diagonal":
+            msgs = diagonal_messages(decomp, rank, spot.radius)
+            acts.append(Action("post", 2, phase=epoch, spot=spot, messages=msgs))
+            acts.append(Action("wait", 0, phase=epoch, spot=spot, messages=msgs))
+            epoch += 1
+            for t in my_interps:
+                acts.append(Action("interp", 0, sparse=t))
+            acts.append(Action("compute", 0, kernel=k, box=domain, region="DOMAIN"))
+        else:  # full: post -> CORE -> wait -> OWNED (Listing 8)
+            msgs = diagonal_messages(decomp, rank, spot.radius)
+            acts.append(Action("post", 2, phase=epoch, spot=spot, messages=msgs))
+            core = rank_regions(decomp, rank, spot.radius, RegionName.CORE)[0]
+            acts.append(Action("compute", 0, kernel=k, box=core, region="CORE"))
+            acts.append(Action("wait", 1, phase=epoch, spot=spot, messages=msgs))
+            epoch += 1
+            for t in my_interps:
+                acts.append(Action("interp", 1, sparse=t))
+            for slab in rank_regions(decomp, rank, spot.radius, RegionName.OWNED):
+                acts.append(Action("compute", 1, kernel=k, box=slab, region="OWNED"))
+            acts.append(Action("record", 1, event=ev))
+            acts.append(Action("streamwait", 0, event=ev))
+            ev += 1
+        for t in my_injects:
+            acts.append(Action("inject", 0, sparse=t))
+    if ev > 32:
+        raise CompilerError("too many stream joins per step")
+    # phases per step is identical on every rank (epoch numbering)
+    per_step = 0
+    for ph in analysis.phases:
+        if ph.halo is not None:
+            per_step += nd if mode == "basic" else 1
+    hoisted_msgs = []
+    if analysis.hoisted is not None:
+        hoisted_msgs = diagonal_messages(decomp, rank, analysis.hoisted.radius)
+    return ExecPlan(mode, acts, max(per_step, 1), analysis.hoisted, hoisted_msgs)

@@ -117,6 +117,22 @@ float* resolve(const sdmp_plan* p, int64_t f, int64_t t, int64_t time) {
   return reinterpret_cast<float*>(fl.ptr[b]);
 }
 
+// Kernel launches one action issues per step (copy-engine copies are not
+// kernel launches).
+int launches_of(const Action& a) {
+  switch ((int)a.i[0]) {
+    case SDMP_ACT_STAR: case SDMP_ACT_EL_V: case SDMP_ACT_EL_T: case SDMP_ACT_VISCO_T:
+    case SDMP_ACT_INJECT: case SDMP_ACT_INTERP: case SDMP_ACT_WAIT:
+      return 1;
+    case SDMP_ACT_TTI:
+      return 2;
+    case SDMP_ACT_POST:
+      return 1 + (a.i[4] == 1 ? (int)a.i[3] : 0);
+    default:
+      return 0;
+  }
+}
+
 int run_action(sdmp_plan* p, const Action& a, int64_t time) {
   const int64_t* I = a.i.data();
   const float* F = a.f.data();
@@ -204,11 +220,11 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
                          ss.series + row * ss.stride);
     }
     case SDMP_ACT_POST: {
-      // [k,s, phase, nmsg, engine, msgs(13 each)..., nsig, (flags_id, slot)...]
+      // [k,s, phase, nmsg, engine, msgs(12 each: fsrc,t,fdst,slo3,dlo3,ext3)..., nsig, (flags_id, slot)...]
       const int64_t phase = I[2], nmsg = I[3];
       const int engine = (int)I[4];
       const int64_t* m = I + 5;
-      for (int64_t q = 0; q < nmsg; ++q, m += 13) {
+      for (int64_t q = 0; q < nmsg; ++q, m += 12) {
         const float* src = resolve(p, m[0], m[1], time);
         float* dst = resolve(p, m[2], m[1], time);
         int rc = copy_box(st, src, p->fields[m[0]].full, m + 3, dst, p->fields[m[2]].full,
@@ -475,12 +491,12 @@ static int validate(const sdmp_plan* p, const Action& a) {
       break;
     case SDMP_ACT_POST: {
       const int64_t nmsg = I[3];
-      SDMP_CHECK(n >= 6 + 13 * nmsg, "post: truncated messages");
+      SDMP_CHECK(n >= 6 + 12 * nmsg, "post: truncated messages");
       const int64_t* m = I + 5;
-      for (int64_t q = 0; q < nmsg; ++q, m += 13)
+      for (int64_t q = 0; q < nmsg; ++q, m += 12)
         SDMP_CHECK(fchk(m[0]) && m[0] >= 0 && fchk(m[2]) && m[2] >= 0, "post: field id");
       const int64_t nsig = *m++;
-      SDMP_CHECK(n >= 6 + 13 * nmsg + 2 * nsig, "post: truncated signals");
+      SDMP_CHECK(n >= 6 + 12 * nmsg + 2 * nsig, "post: truncated signals");
       for (int64_t q = 0; q < nsig; ++q)
         SDMP_CHECK(m[2 * q] >= 0 && m[2 * q] < (int64_t)p->flags.size() && m[2 * q + 1] >= 0 &&
                        m[2 * q + 1] < 32, "post: flags id / slot");
@@ -516,17 +532,23 @@ extern "C" int sdmp_plan_set_timeout(sdmp_plan* p, int64_t ms) {
 
 extern "C" int sdmp_plan_set_tracing(sdmp_plan* p, int32_t on) {
   SDMP_CHECK(p, "null plan");
-  SDMP_CUDA(cudaSetDevice(p->device));
   p->tracing = on != 0;
-  if (p->tracing) {
-    while (p->tr_beg.size() < p->actions.size()) {
-      cudaEvent_t b, e;
-      SDMP_CUDA(cudaEventCreate(&b));
-      SDMP_CUDA(cudaEventCreate(&e));
-      p->tr_beg.push_back(b);
-      p->tr_end.push_back(e);
-    }
-    if (!p->tr_origin) SDMP_CUDA(cudaEventCreate(&p->tr_origin));
+  return SDMP_OK;
+}
+
+// events for (step s, action k): begin at 2*(s*nact+k), end at +1; one
+// origin event per step (recorded on stream 0 at the step start)
+static int trace_events(sdmp_plan* p, int64_t steps) {
+  const size_t need = (size_t)(2 * steps * p->actions.size());
+  while (p->tr_beg.size() < need) {
+    cudaEvent_t e;
+    SDMP_CUDA(cudaEventCreate(&e));
+    p->tr_beg.push_back(e);
+  }
+  while (p->tr_end.size() < (size_t)steps) {
+    cudaEvent_t e;
+    SDMP_CUDA(cudaEventCreate(&e));
+    p->tr_end.push_back(e);
   }
   return SDMP_OK;
 }
@@ -545,28 +567,34 @@ extern "C" int sdmp_plan_run(sdmp_plan* p, int64_t time_m, int64_t time_M, void*
   SDMP_CHECK(time_M >= time_m - 1, "time_M < time_m - 1");
   SDMP_CUDA(cudaSetDevice(p->device));
   cudaStream_t user = (cudaStream_t)stream;
+  const int64_t nsteps = time_M - time_m + 1;
+  const size_t nact = p->actions.size();
+  if (p->tracing && nsteps > 0) {
+    int rc = trace_events(p, nsteps);
+    if (rc) return rc;
+  }
   SDMP_CUDA(cudaEventRecord(p->ev_in, user));
   SDMP_CUDA(cudaStreamWaitEvent(p->s[0], p->ev_in, 0));
   for (int64_t time = time_m; time <= time_M; ++time) {
-    const bool trace = p->tracing && time == time_M;
+    const int64_t si = time - time_m;
     SDMP_CUDA(cudaEventRecord(p->ev_step, p->s[0]));
     SDMP_CUDA(cudaStreamWaitEvent(p->s[1], p->ev_step, 0));
     SDMP_CUDA(cudaStreamWaitEvent(p->s[2], p->ev_step, 0));
-    if (trace) SDMP_CUDA(cudaEventRecord(p->tr_origin, p->s[0]));
-    for (size_t k = 0; k < p->actions.size(); ++k) {
+    if (p->tracing) SDMP_CUDA(cudaEventRecord(p->tr_end[si], p->s[0]));
+    for (size_t k = 0; k < nact; ++k) {
       cudaStream_t st = p->s[p->actions[k].i[1]];
-      if (trace) SDMP_CUDA(cudaEventRecord(p->tr_beg[k], st));
+      if (p->tracing) SDMP_CUDA(cudaEventRecord(p->tr_beg[2 * (si * nact + k)], st));
       int rc = run_action(p, p->actions[k], time);
       if (rc) return rc;
-      if (trace) SDMP_CUDA(cudaEventRecord(p->tr_end[k], st));
+      if (p->tracing) SDMP_CUDA(cudaEventRecord(p->tr_beg[2 * (si * nact + k) + 1], st));
     }
     SDMP_CUDA(cudaEventRecord(p->ev_join[1], p->s[1]));
     SDMP_CUDA(cudaEventRecord(p->ev_join[2], p->s[2]));
     SDMP_CUDA(cudaStreamWaitEvent(p->s[0], p->ev_join[1], 0));
     SDMP_CUDA(cudaStreamWaitEvent(p->s[0], p->ev_join[2], 0));
     p->steps_done += 1;
-    if (trace) p->last_traced = (int)p->actions.size();
   }
+  p->last_traced = p->tracing ? (int)nsteps : 0;
   SDMP_CUDA(cudaEventRecord(p->ev_out, p->s[0]));
   SDMP_CUDA(cudaStreamWaitEvent(user, p->ev_out, 0));
   return SDMP_OK;
@@ -585,19 +613,30 @@ extern "C" int sdmp_plan_sync(sdmp_plan* p) {
   return SDMP_OK;
 }
 
+// rows (6 per action): {index, stream, kind, mean start ms (from the step
+// start on stream 0), mean duration ms, launches per step}, averaged over
+// every step of the last traced run.
 extern "C" int sdmp_plan_trace(sdmp_plan* p, double* rows, int32_t max_rows, int32_t* nrows) {
   SDMP_CHECK(p && rows && nrows, "null argument");
   SDMP_CUDA(cudaSetDevice(p->device));
+  const int64_t nsteps = p->last_traced;
+  const size_t nact = p->actions.size();
   int n = 0;
-  for (int k = 0; k < p->last_traced && n < max_rows; ++k, ++n) {
-    float b = 0.f, e = 0.f;
-    SDMP_CUDA(cudaEventElapsedTime(&b, p->tr_origin, p->tr_beg[k]));
-    SDMP_CUDA(cudaEventElapsedTime(&e, p->tr_origin, p->tr_end[k]));
-    rows[5 * n + 0] = k;
-    rows[5 * n + 1] = (double)p->actions[k].i[1];
-    rows[5 * n + 2] = (double)p->actions[k].i[0];
-    rows[5 * n + 3] = b;
-    rows[5 * n + 4] = e;
+  for (size_t k = 0; k < nact && n < max_rows && nsteps > 0; ++k, ++n) {
+    double sb = 0.0, sd = 0.0;
+    for (int64_t s = 0; s < nsteps; ++s) {
+      float b = 0.f, e = 0.f;
+      SDMP_CUDA(cudaEventElapsedTime(&b, p->tr_end[s], p->tr_beg[2 * (s * nact + k)]));
+      SDMP_CUDA(cudaEventElapsedTime(&e, p->tr_end[s], p->tr_beg[2 * (s * nact + k) + 1]));
+      sb += b;
+      sd += e - b;
+    }
+    rows[6 * n + 0] = (double)k;
+    rows[6 * n + 1] = (double)p->actions[k].i[1];
+    rows[6 * n + 2] = (double)p->actions[k].i[0];
+    rows[6 * n + 3] = sb / nsteps;
+    rows[6 * n + 4] = sd / nsteps;
+    rows[6 * n + 5] = (double)launches_of(p->actions[k]);
   }
   *nrows = n;
   return SDMP_OK;

@@ -273,11 +273,13 @@ class NativePlan:
         check(lib().sdmp_plan_set_timeout(self.h, int(ms)), "sdmp_plan_set_timeout", self.rank)
 
     def trace(self, max_rows: int = 512):
-        rows = (C.c_double * (5 * max_rows))()
+        """Per-action rows (index, stream, kind, mean start ms, mean duration
+        ms, kernel launches per step) averaged over the last traced run."""
+        rows = (C.c_double * (6 * max_rows))()
         n = C.c_int32(0)
         check(lib().sdmp_plan_trace(self.h, rows, max_rows, C.byref(n)), "sdmp_plan_trace",
               self.rank)
-        return [tuple(rows[5 * i: 5 * i + 5]) for i in range(n.value)]
+        return [tuple(rows[6 * i: 6 * i + 6]) for i in range(n.value)]
 
     def close(self):
         if self.h:

