@@ -150,7 +150,8 @@ class Data:
             # the part of the value that lands on this rank
             sub = tuple(slice(l + e0 - r0, h + e0 - r0) for (l, h), (e0, _e1), (r0, _r1)
                         in zip(loc, ext, region))
-            val = torch.from_numpy(np.ascontiguousarray(val[sub])).to(fn.storage.device)
+            val = torch.from_numpy(np.array(val[sub], dtype=np.float32, order="C")).to(
+                fn.storage.device)
             if fn.grid.ndims == 2:
                 val = val.unsqueeze(-1)
         for b in self._buffers(tsel, True):

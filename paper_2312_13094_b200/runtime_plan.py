@@ -187,7 +187,7 @@ class NativeOperatorPlan:
         elif a.kind == "streamwait":
             P.add_action([R.ACT["STREAMWAIT"], a.stream, a.event])
         elif a.kind == "inject":
-            sid, mid, C = self.sparse_sets[id(a.sparse)]
+            sid, mid, C = self.sparse_sets[id(a.sparse)][:3]
             P.add_action([R.ACT["INJECT"], a.stream, self.fid[a.sparse.field], 1, mid, sid], [C])
         elif a.kind == "interp":
             sid = self.sparse_sets[id(a.sparse)][0]
