@@ -226,6 +226,9 @@ class NativePlan:
               "sdmp_plan_create", rank)
         self.h = h
         self._keep = []  # keep device arrays referenced for the plan lifetime
+        ms = os.environ.get("SDMP_TIMEOUT_MS")
+        if ms:
+            self.set_timeout(int(ms))
 
     def add_field(self, ptrs: Sequence[int], full: Sequence[int]) -> int:
         fid = C.c_int32(0)
