@@ -260,7 +260,7 @@ def main():
     comp = [(i, a) for i, a in enumerate(ep.actions) if a.kind == "compute"]
     big_i, big_a = max(comp, key=lambda ia: math.prod(h_ - l_ for l_, h_ in zip(*ia[1].box)))
     big_pts = math.prod(h_ - l_ for l_, h_ in zip(*big_a.box))
-    big_ms = rows[big_i][4]
+    big_ms = rows[plan.native_index[big_i]][4]
     bpp = big_a.kernel.bytes_per_point
     peak, peak_src = load_peaks()
     achieved = bpp * big_pts / (big_ms * 1e-3) / 1e9
@@ -292,8 +292,29 @@ def main():
     except Exception as exc:  # pragma: no cover
         e2e = {"value": None, "error": str(exc)[:200]}
 
-    # exposed halo time (N > 1): same decomposition, compute only
+    # exposed halo time (N > 1): same decomposition and boxes, compute only
     exposed = None
+    if N > 1:
+        cplan = op._native(mode, dt, exchange=False)
+        cplan.run(0, 1)
+        ctx.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        cplan.plan.run(2, args.steps + 1, stream)
+        e1.record(stream)
+        cplan.plan.sync()
+        torch.cuda.synchronize()
+        ms_c = ctx.allreduce_max(e0.elapsed_time(e1))
+        posts = [(i, a) for i, a in enumerate(ep.actions) if a.kind == "post" and a.messages]
+        sent = sum(m.volume for _i, a in posts for m in a.messages) * 4
+        post_ms = sum(rows[plan.native_index[i]][4] for i, _a in posts)
+        exposed = {"exposed_ms_per_step": (ms_max - ms_c) / args.steps,
+                   "step_ms": ms_max / args.steps, "compute_only_step_ms": ms_c / args.steps,
+                   "exposed_frac": (ms_max - ms_c) / ms_max,
+                   "halo_bytes_sent_per_step_rank0": sent,
+                   "post_ms_rank0": post_ms,
+                   "link_gbs_rank0": sent / (post_ms * 1e-3) / 1e9 if post_ms > 0 else None,
+                   "link_peak_gbs": 900.0}
 
     cpu = None
     if ctx.rank == 0 and N == 1 and not args.no_cpu_baseline:
@@ -322,7 +343,7 @@ def main():
             "gpu_launches": launches,
             "e2e": e2e,
             "clocks": clk,
-            "exposed_halo_ms_per_step": exposed,
+            "halo": exposed,
             "cpu_baseline": cpu,
             "step_actions": [{"kind": int(r[2]), "stream": int(r[1]),
                               "ms": round(r[4], 4)} for r in rows],

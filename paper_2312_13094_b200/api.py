@@ -511,18 +511,18 @@ class Operator:
         self.last_summary = None
 
     # ------------------------------------------------------------------
-    def plan(self, mode=None, dt=None):
+    def plan(self, mode=None, dt=None, exchange=True):
         """The per-rank ExecPlan (host description; used by tests)."""
         mode = CP.normalise_mode(mode or _env_mode())
         an = CP.halo_phases(self.kernels, self.grid.decomposition.nranks)
         return CP.lower_mode(an, self.grid.decomposition, self.grid.rank, mode,
-                             self.sparse_terms)
+                             self.sparse_terms, exchange=exchange)
 
-    def _native(self, mode, dt):
-        key = (mode, None if dt is None else float(np.float32(dt)))
+    def _native(self, mode, dt, exchange=True):
+        key = (mode, None if dt is None else float(np.float32(dt)), exchange)
         if key not in self._plans:
             from .runtime_plan import NativeOperatorPlan
-            self._plans[key] = NativeOperatorPlan(self, mode, dt)
+            self._plans[key] = NativeOperatorPlan(self, mode, dt, exchange=exchange)
         return self._plans[key]
 
     def apply(self, time_m: int = 0, time_M: Optional[int] = None, dt=None, mpi=None,

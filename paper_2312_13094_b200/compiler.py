@@ -414,8 +414,12 @@ class ExecPlan:
 
 
 def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
-               sparse_terms: Sequence = ()) -> ExecPlan:
-    """Per-rank ExecPlan for ``mode``."""
+               sparse_terms: Sequence = (), exchange: bool = True) -> ExecPlan:
+    """Per-rank ExecPlan for ``mode``.
+
+    ``exchange=False`` keeps the mode's compute boxes and stream structure
+    but drops every post/wait: the compute-only baseline used to measure
+    the exposed halo-exchange time per step."""
     from .distfield import (RegionName, basic_messages, diagonal_messages,
                             rank_regions)
 
@@ -488,6 +492,8 @@ def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
             acts.append(Action("inject", 0, sparse=t))
     if ev > 32:
         raise CompilerError("too many stream joins per step")
+    if not exchange:
+        acts = [a for a in acts if a.kind not in ("post", "wait")]
     # phases per step is identical on every rank (epoch numbering)
     per_step = 0
     for ph in analysis.phases:

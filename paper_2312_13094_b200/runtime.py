@@ -226,6 +226,7 @@ class NativePlan:
               "sdmp_plan_create", rank)
         self.h = h
         self._keep = []  # keep device arrays referenced for the plan lifetime
+        self.nact = 0
         ms = os.environ.get("SDMP_TIMEOUT_MS")
         if ms:
             self.set_timeout(int(ms))
@@ -261,6 +262,7 @@ class NativePlan:
         fl = arr_f32(floats) if len(floats) else None
         check(lib().sdmp_plan_add_action(self.h, arr_i64(ints), len(ints), fl, len(floats)),
               "sdmp_plan_add_action", self.rank)
+        self.nact += 1
 
     def run(self, time_m: int, time_M: int, stream=None):
         check(lib().sdmp_plan_run(self.h, int(time_m), int(time_M), C.c_void_p(stream_handle(stream))),

@@ -58,7 +58,7 @@ def staggered_binding(k: CP.StaggeredPhase, spacing, dt):
 
 
 class NativeOperatorPlan:
-    def __init__(self, op, mode: str, dt):
+    def __init__(self, op, mode: str, dt, exchange: bool = True):
         torch = __import__("torch")
         self.op = op
         self.mode = mode
@@ -67,7 +67,7 @@ class NativeOperatorPlan:
         self.ctx = ctx = grid.ctx
         self.rank = rank = ctx.rank
         decomp = grid.decomposition
-        self.eplan = op.plan(mode, dt)
+        self.eplan = op.plan(mode, dt, exchange=exchange)
         ep = self.eplan
         self.plan = R.NativePlan(ctx.device or 0, ep.phases_per_step, rank)
         self.static = None
@@ -159,6 +159,7 @@ class NativeOperatorPlan:
             self._add_sparse(t, decomp, rank)
 
         # -- actions --------------------------------------------------------
+        self.native_index = []
         for a in ep.actions:
             self._encode(a, decomp, rank)
         if need_static:
@@ -174,14 +175,21 @@ class NativeOperatorPlan:
 
     def _encode(self, a: CP.Action, decomp, rank):
         P = self.plan
+        # ExecPlan action -> index of its native action (-1: nothing to do)
+        self.native_index.append(self.plan.nact)
         if a.kind == "compute":
             P.add_action(*self._compute_ints(a.kernel, a.box, a.stream))
         elif a.kind == "post":
+            if not a.messages:
+                self.native_index[-1] = -1
+                return
             P.add_action(self._post_ints(a, self.fid, self.pfid, self.pflag, decomp, rank))
         elif a.kind == "wait":
             slots = sorted({direction_slot(m.direction) for m in a.messages})
-            if slots:
-                P.add_action([R.ACT["WAIT"], a.stream, a.phase, len(slots)] + slots)
+            if not slots:
+                self.native_index[-1] = -1
+                return
+            P.add_action([R.ACT["WAIT"], a.stream, a.phase, len(slots)] + slots)
         elif a.kind == "record":
             P.add_action([R.ACT["RECORD"], a.stream, a.event])
         elif a.kind == "streamwait":
