@@ -1,0 +1,147 @@
+"""Host-side compiler: family recognition by exact probing, HaloSpot
+optimisation (drop / merge / hoist), ExecPlan structure per mode
+(acceptance 4, 5, 8) and the C-ABI surface."""
+import os
+import re
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from paper_2312_13094_b200 import compiler as CP
+from paper_2312_13094_b200 import decomposition as DC
+from paper_2312_13094_b200 import symbolics as S
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def acoustic_eq(so, nd=3, n=16):
+    g = S.GridSpec((n,) * nd, (10.0 * (n - 1),) * nd)
+    u = S.FieldSpec("u", g, so, 2)
+    m = S.FieldSpec("m", g, so, 0)
+    return S.solve_forward(S.Eq(m.at() * u.dt2 - u.laplace), u.forward), u, m
+
+
+@pytest.mark.parametrize("so", [2, 4, 6, 8, 12, 16])
+@pytest.mark.parametrize("nd", [2, 3])
+def test_recognise_acoustic(so, nd):
+    eq, u, m = acoustic_eq(so, nd)
+    k = CP.recognise([eq])[0]
+    assert isinstance(k, CP.StarKernel)
+    assert (k.A, k.B, k.c, k.p, k.q) == (2, -1, 1, 2, -1)
+    assert k.m == m and k.radius == (so // 2,) * nd
+    assert k.weights[0] == tuple(S.fd_coefficients(2, so)[so // 2:])
+
+
+def test_recognise_diffusion_and_variants():
+    g = S.GridSpec((8, 8), (2.0, 2.0))
+    u = S.FieldSpec("u", g, 2, 1)
+    k = CP.recognise([S.solve_forward(S.Eq(u.dt, u.laplace), u.forward)])[0]
+    assert (k.A, k.B, k.c, k.p, k.q, k.m) == (1, 0, 1, 1, 0, None)
+    # scaled diffusion u.dt = 3 * lap -> c = 3
+    k = CP.recognise([S.solve_forward(S.Eq(u.dt, 3 * u.laplace), u.forward)])[0]
+    assert (k.A, k.c, k.p) == (1, 3, 1)
+    # heat with coefficient: m u.dt = lap -> S = dt / m
+    m = S.FieldSpec("m", g, 2, 0)
+    k = CP.recognise([S.solve_forward(S.Eq(m.at() * u.dt, u.laplace), u.forward)])[0]
+    assert (k.p, k.q, k.m) == (1, -1, m)
+
+
+def test_recognise_rejects_unsupported():
+    g = S.GridSpec((8, 8), (2.0, 2.0))
+    u = S.FieldSpec("u", g, 2, 1)
+    for eq in [S.Eq(u.dt, u.dx), S.Eq(u.dt, u.laplace + u.dx)]:
+        with pytest.raises(CP.CompilerError):
+            CP.recognise([S.solve_forward(eq, u.forward)])
+
+
+def test_halospots_drop_merge_hoist():
+    eq, u, m = acoustic_eq(8)
+    k = CP.recognise([eq])[0]
+    an = CP.halo_phases([k, k], nranks=4)
+    # two consecutive readers of u[t0] without a write in between -> 1 spot
+    assert an.phases[0].halo is not None and an.phases[1].halo is None
+    assert an.exchanges_per_step == 1
+    # single rank -> no spots at all
+    assert CP.halo_phases([k], nranks=1).exchanges_per_step == 0
+    # TTI: read-only direction cosines hoisted out of the time loop
+    g = S.GridSpec((16,) * 3, (150.0,) * 3)
+    f = lambda n, to=0: S.FieldSpec(n, g, 8, to)
+    tti = CP.TTIKernel(f("p", 2), f("r", 2), f("mt"), f("e"), f("d"),
+                       (f("ax"), f("ay"), f("az")), 8)
+    an = CP.halo_phases([tti], nranks=2)
+    assert an.hoisted is not None and {x[0].name for x in an.hoisted.fields} == {"ax", "ay", "az"}
+    assert an.hoisted.radius == (4, 4, 4)
+    assert an.phases[0].halo.radius == (8, 8, 8)
+    assert {x[0].name for x in an.phases[0].halo.fields} == {"p", "r"}
+
+
+def test_elastic_two_exchanges_per_step():
+    g = S.GridSpec((16,) * 3, (150.0,) * 3)
+    v = tuple(S.FieldSpec(n, g, 8, 1) for n in ("vx", "vy", "vz"))
+    t = tuple(S.FieldSpec(n, g, 8, 1) for n in ("txx", "tyy", "tzz", "txy", "txz", "tyz"))
+    b, lam, mu = (S.FieldSpec(n, g, 8, 0) for n in ("b", "lam", "mu"))
+    kv = CP.StaggeredPhase("v", v, t, (b,), so=8)
+    kt = CP.StaggeredPhase("t", v, t, (lam, mu), so=8)
+    an = CP.halo_phases([kv, kt], nranks=8)
+    assert an.exchanges_per_step == 2
+    assert [x[1] for x in an.phases[0].halo.fields] == [0] * 6   # tau[t0] before v
+    assert [x[1] for x in an.phases[1].halo.fields] == [1] * 3   # v[t1] before tau
+
+
+def plan_for(mode, dims=(2, 2, 1), rank=0, shape=(32, 32, 32)):
+    eq, u, m = acoustic_eq(8, 3, 32)
+    k = CP.recognise([eq])[0]
+    d = DC.Decomposition.create(shape, int(np.prod(dims)), dims)
+    an = CP.halo_phases([k], d.nranks)
+    return CP.lower_mode(an, d, rank, mode)
+
+
+def test_full_mode_listing8_order():
+    p = plan_for("full")
+    kinds = [a.kind if a.kind != "compute" else a.region for a in p.actions]
+    post, core, wait = kinds.index("post"), kinds.index("CORE"), kinds.index("wait")
+    owned = [i for i, k in enumerate(kinds) if k == "OWNED"]
+    assert post < core < wait < min(owned)  # Listing 8 (acceptance 8)
+    core_a = p.actions[core]
+    wait_a = p.actions[wait]
+    assert core_a.stream != wait_a.stream  # CORE overlaps the exchange
+    assert p.phases_per_step == 1
+
+
+def test_basic_and_diagonal_structure():
+    b = plan_for("basic")
+    posts = [a for a in b.actions if a.kind == "post"]
+    assert len(posts) == 3 and b.phases_per_step == 3  # axis-sequenced x, y, z
+    assert [len(a.messages) for a in posts] == [1, 1, 0]
+    d = plan_for("diagonal")
+    assert [len(a.messages) for a in d.actions if a.kind == "post"] == [3]
+    assert [a.region for a in d.actions if a.kind == "compute"] == ["DOMAIN"]
+
+
+def test_interior_message_counts_3d():
+    for mode, want in (("basic", 6), ("diagonal", 26), ("full", 26)):
+        p = plan_for(mode, dims=(3, 3, 3), rank=13, shape=(48, 48, 48))
+        assert p.message_count() == want
+
+
+def test_mode_aliases():
+    assert CP.normalise_mode("diag2") == "diagonal"
+    assert CP.normalise_mode("1") == "basic"
+    assert CP.normalise_mode("FULL") == "full"
+    with pytest.raises(CP.CompilerError):
+        CP.normalise_mode("nope")
+
+
+def test_c_abi_library_exports_every_declared_symbol():
+    from paper_2312_13094_b200 import runtime as R
+    lib = R.lib()
+    with open(os.path.join(ROOT, "include", "sdmp.h")) as f:
+        declared = set(re.findall(r"\b(sdmp_[a-z0-9_]+)\s*\(", f.read()))
+    assert len(declared) >= 30
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+    assert lib.sdmp_version() == 1
+    # error path without touching a GPU
+    assert lib.sdmp_plan_add_action(None, None, 0, None, 0) == -1
+    assert b"null" in lib.sdmp_last_error()
