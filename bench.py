@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--so", type=int, default=8)
     ap.add_argument("--n", type=int, default=1024, help="grid points per axis per GPU")
     ap.add_argument("--nrec", type=int, default=256)
+    ap.add_argument("--kernel", default="acoustic", choices=["acoustic", "tti", "elastic", "visco"])
+    ap.add_argument("--shape", default=None, help="override the global shape nx,ny,nz")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -214,17 +216,41 @@ def main():
     topo = TOPOS[N]
     n = args.n
     shape = tuple(n * p for p in topo)
+    if args.shape:
+        shape = tuple(int(x) for x in args.shape.split(","))
     h = 10.0
     grid = Grid(shape, tuple(h * (s - 1) for s in shape), topology=topo)
-    kd = KD.acoustic_model(grid, so=args.so)
-    u, m = kd.fields["u"], kd.fields["m"]
-    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing)))
     total_steps = args.warmup + args.steps
     nt = total_steps + 1
     ext = grid.extent
-    src = KD.point_source(grid, [tuple(0.5 * e + 3.7 for e in ext)], nt, dt, f0=0.010)
+    src = KD.point_source(grid, [tuple(0.5 * e + 3.7 for e in ext)], nt, 1.0, f0=0.010)
     rec = KD.receiver_line(grid, args.nrec, nt)
-    op = Operator([kd, src.inject(u.forward, expr=src * S.DT ** 2 / m), rec.interpolate(u)])
+    kname = args.kernel
+    if kname == "acoustic":
+        kd = KD.acoustic_model(grid, so=args.so)
+        u, m = kd.fields["u"], kd.fields["m"]
+        dt = float(np.float32(KD.critical_dt(4.6, grid.spacing)))
+        terms = [src.inject(u.forward, expr=src * S.DT ** 2 / m), rec.interpolate(u)]
+    elif kname == "tti":
+        kd = KD.tti_model(grid, so=args.so)
+        p, r, m = kd.fields["p"], kd.fields["r"], kd.fields["m"]
+        dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.25)))
+        src2 = KD.point_source(grid, src.coordinates, nt, 1.0, f0=0.010, name="src_r")
+        terms = [src.inject(p.forward, expr=src * S.DT ** 2 / m),
+                 src2.inject(r.forward, expr=src2 * S.DT ** 2 / m), rec.interpolate(p)]
+    else:
+        kd = (KD.viscoelastic_model(grid, so=args.so) if kname == "visco"
+              else KD.elastic_model(grid, so=args.so))
+        dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.15)))
+        terms = []
+        for c in ("txx", "tyy", "tzz"):
+            sc = KD.point_source(grid, src.coordinates, nt, 1.0, f0=0.010, name=f"src_{c}")
+            terms.append(sc.inject(kd.fields[c].forward, expr=sc * S.DT))
+        terms.append(rec.interpolate(kd.fields["vz"]))
+    srcs = [t.sparse for t in terms if t.kind == "inject"]
+    for s_ in srcs:  # Ricker sampled on this dt
+        s_.data[:] = np.float32(KD.ricker(0.010, np.arange(nt) * dt, 100.0))[:, None]
+    op = Operator([kd] + terms)
     mode = args.mode
 
     # ---- device-timed region: the native plan replays K steps ------------
@@ -258,9 +284,16 @@ def main():
     # dominant kernel: the largest compute action (CORE in full, DOMAIN else)
     ep = plan.eplan
     comp = [(i, a) for i, a in enumerate(ep.actions) if a.kind == "compute"]
-    big_i, big_a = max(comp, key=lambda ia: math.prod(h_ - l_ for l_, h_ in zip(*ia[1].box)))
+    # longest compute action of the step (per-action CUDA-event means)
+    big_i, big_a = max(comp, key=lambda ia: rows[plan.native_index[ia[0]]][4])
     big_pts = math.prod(h_ - l_ for l_, h_ in zip(*big_a.box))
     big_ms = rows[plan.native_index[big_i]][4]
+    kernel_label = {"acoustic": f"star_tma<{args.so // 2}> (acoustic SO-{args.so}, TMA pipeline)",
+                    "tti": f"tti_g + tti_update (SO-{args.so})",
+                    "elastic": f"el_velocity / el_stress (SO-{args.so})",
+                    "visco": f"el_velocity / visco_stress (SO-{args.so})"}[kname]
+    if kname in ("elastic", "visco"):
+        kernel_label += f" [{big_a.kernel.kind} phase]"
     bpp = big_a.kernel.bytes_per_point
     peak, peak_src = load_peaks()
     achieved = bpp * big_pts / (big_ms * 1e-3) / 1e9
@@ -269,7 +302,7 @@ def main():
     if os.path.exists(prof):
         try:
             d = json.load(open(prof))
-            key = f"acoustic_so{args.so}_{n}"
+            key = f"{kname}_so{args.so}_{n}" if not args.shape else f"{kname}_so{args.so}_{args.shape}"
             if key in d:
                 traffic = d[key].get("dram_bytes_per_launch")
         except Exception:
@@ -329,15 +362,16 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
             "data": "synthetic (layered vp + hashed noise, Ricker source, receiver line)",
-            "config": {"workload": f"3D isotropic acoustic SO-{args.so}, {n}^3 per GPU "
-                                   "(BASELINE configs[1])",
+            "config": {"workload": (f"3D isotropic acoustic SO-{args.so}, {n}^3 per GPU "
+                                    "(BASELINE configs[1])") if kname == "acoustic" and not args.shape
+                       else f"3D {kname} SO-{args.so}, global {shape}",
                        "global_shape": list(shape), "topology": list(topo), "mode": mode,
                        "parallelism": f"domain decomposition x/y {topo}",
                        "sources": 1, "receivers": args.nrec,
                        "l2": "no flush: every array (4.5 GB) >> 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "star_tma (acoustic SO-8, TMA pipeline)",
+                         "kernel": kernel_label,
                          "bytes_per_point": bpp, "points_per_launch": big_pts,
                          "launch_ms": big_ms, "peak_source": peak_src},
             "gpu_launches": launches,

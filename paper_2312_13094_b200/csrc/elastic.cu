@@ -7,127 +7,265 @@
 // normal stresses at nodes, shear stresses on edges (Virieux 1986):
 //   D+ f(i) = sum_k c_k (f[i+k] - f[i-k+1])   (derivative at i+1/2)
 //   D- f(i) = sum_k c_k (f[i+k-1] - f[i-k])   (derivative at i-1/2)
-// Each phase reads its neighbours through L1/L2 (one thread per point,
-// z-fastest warps -> coalesced rows).  Per-point arithmetic uses explicit
-// _rn intrinsics so every launch geometry gives identical bits.
+//
+// Two launch shapes share ONE per-point routine (templated on an accessor):
+//  * generic: one thread per point, taps through L1/L2 (thin OWNED slabs,
+//    unaligned boxes);
+//  * stream: the TMA streaming engine (stream.cuh) — x taps from per-field
+//    register windows, y/z taps from staged halo tiles, pointwise operands
+//    from staged tiles; every array crosses HBM once per phase.
+#include <cstdlib>
+
 #include "common.cuh"
+#include "stream.cuh"
 
 namespace sdmp {
 
-struct ElParams {
-  const float* __restrict__ in[16];
-  float* __restrict__ out[12];
-  Geom g;
+struct ElCoef {
   float c[3][SDMP_MAX_RADIUS];
   float dt;
 };
 
-template <int R>
-__device__ __forceinline__ float dplus(const float* __restrict__ f, int64_t i, int64_t s,
-                                       const float* c) {
-  float acc = __fmul_rn(c[0], __fsub_rn(__ldg(f + i + s), __ldg(f + i)));
+// logical field ids
+enum { TXX = 0, TYY, TZZ, TXY, TXZ, TYZ, VX, VY, VZ, PB, NV_ = 10 };
+
+template <int R, int AX, int F, class A>
+__device__ __forceinline__ float dplus(const A& a, const float* c) {
+  float acc = __fmul_rn(c[0], __fsub_rn(a.template t<F, AX>(1), a.template t<F, AX>(0)));
 #pragma unroll
   for (int k = 2; k <= R; ++k)
-    acc = __fmaf_rn(c[k - 1], __fsub_rn(__ldg(f + i + k * s), __ldg(f + i - (k - 1) * s)), acc);
+    acc = __fmaf_rn(c[k - 1], __fsub_rn(a.template t<F, AX>(k), a.template t<F, AX>(1 - k)), acc);
   return acc;
 }
 
-template <int R>
-__device__ __forceinline__ float dminus(const float* __restrict__ f, int64_t i, int64_t s,
-                                        const float* c) {
-  float acc = __fmul_rn(c[0], __fsub_rn(__ldg(f + i), __ldg(f + i - s)));
+template <int R, int AX, int F, class A>
+__device__ __forceinline__ float dminus(const A& a, const float* c) {
+  float acc = __fmul_rn(c[0], __fsub_rn(a.template t<F, AX>(0), a.template t<F, AX>(-1)));
 #pragma unroll
   for (int k = 2; k <= R; ++k)
-    acc = __fmaf_rn(c[k - 1], __fsub_rn(__ldg(f + i + (k - 1) * s), __ldg(f + i - k * s)), acc);
+    acc = __fmaf_rn(c[k - 1], __fsub_rn(a.template t<F, AX>(k - 1), a.template t<F, AX>(-k)), acc);
   return acc;
 }
+
+// ---- per-point routines (shared by both launch shapes) --------------------
+
+template <int R, class A>
+__device__ __forceinline__ void vel_point(const A& a, const ElCoef& k, float out[3]) {
+  const float bdt = __fmul_rn(k.dt, a.template p<PB>());
+  float dvx = __fadd_rn(__fadd_rn(dplus<R, 0, TXX>(a, k.c[0]), dminus<R, 1, TXY>(a, k.c[1])),
+                        dminus<R, 2, TXZ>(a, k.c[2]));
+  float dvy = __fadd_rn(__fadd_rn(dminus<R, 0, TXY>(a, k.c[0]), dplus<R, 1, TYY>(a, k.c[1])),
+                        dminus<R, 2, TYZ>(a, k.c[2]));
+  float dvz = __fadd_rn(__fadd_rn(dminus<R, 0, TXZ>(a, k.c[0]), dminus<R, 1, TYZ>(a, k.c[1])),
+                        dplus<R, 2, TZZ>(a, k.c[2]));
+  out[0] = __fmaf_rn(bdt, dvx, a.template p<VX>());
+  out[1] = __fmaf_rn(bdt, dvy, a.template p<VY>());
+  out[2] = __fmaf_rn(bdt, dvz, a.template p<VZ>());
+}
+
+// strains from v (logical VX, VY, VZ): exx, eyy, ezz, exy, exz, eyz
+template <int R, class A>
+__device__ __forceinline__ void strain_point(const A& a, const ElCoef& k, float e[6]) {
+  e[0] = dminus<R, 0, VX>(a, k.c[0]);
+  e[1] = dminus<R, 1, VY>(a, k.c[1]);
+  e[2] = dminus<R, 2, VZ>(a, k.c[2]);
+  e[3] = __fadd_rn(dplus<R, 1, VX>(a, k.c[1]), dplus<R, 0, VY>(a, k.c[0]));
+  e[4] = __fadd_rn(dplus<R, 2, VX>(a, k.c[2]), dplus<R, 0, VZ>(a, k.c[0]));
+  e[5] = __fadd_rn(dplus<R, 2, VY>(a, k.c[2]), dplus<R, 1, VZ>(a, k.c[1]));
+}
+
+// logical pointwise ids of the stress phases
+enum { S0 = 0, LAM = 6, MU = 7, R0 = 8, L2M = 14, MUS = 15, ITS = 16 };
+
+template <int R, class A>
+__device__ __forceinline__ void stress_point(const A& a, const ElCoef& k, float out[6]) {
+  float e[6];
+  strain_point<R>(a, k, e);
+  const float l = a.template q<LAM>(), mu = a.template q<MU>();
+  const float tr = __fadd_rn(__fadd_rn(e[0], e[1]), e[2]);
+  const float ltr = __fmul_rn(l, tr), m2 = __fmul_rn(2.f, mu);
+  out[0] = __fmaf_rn(k.dt, __fmaf_rn(m2, e[0], ltr), a.template q<S0 + 0>());
+  out[1] = __fmaf_rn(k.dt, __fmaf_rn(m2, e[1], ltr), a.template q<S0 + 1>());
+  out[2] = __fmaf_rn(k.dt, __fmaf_rn(m2, e[2], ltr), a.template q<S0 + 2>());
+  out[3] = __fmaf_rn(k.dt, __fmul_rn(mu, e[3]), a.template q<S0 + 3>());
+  out[4] = __fmaf_rn(k.dt, __fmul_rn(mu, e[4]), a.template q<S0 + 4>());
+  out[5] = __fmaf_rn(k.dt, __fmul_rn(mu, e[5]), a.template q<S0 + 5>());
+}
+
+template <int C, class A>
+__device__ __forceinline__ void visco_comp(const A& a, const ElCoef& k, const float e[6],
+                                           float base, float m2, float M, float dti, float* s1,
+                                           float* r1) {
+  const float Ac = C < 3 ? __fmaf_rn(m2, e[C], base) : __fmul_rn(M, e[C]);
+  const float r0v = a.template q<R0 + C>();
+  const float rn = __fmaf_rn(-dti, __fadd_rn(r0v, Ac), r0v);
+  r1[C] = rn;
+  s1[C] = __fmaf_rn(k.dt, __fadd_rn(Ac, rn), a.template q<S0 + C>());
+}
+
+template <int R, class A>
+__device__ __forceinline__ void visco_point(const A& a, const ElCoef& k, float s1[6],
+                                            float r1[6]) {
+  float e[6];
+  strain_point<R>(a, k, e);
+  const float L = a.template q<L2M>(), M = a.template q<MUS>(), I = a.template q<ITS>();
+  const float div = __fadd_rn(__fadd_rn(e[0], e[1]), e[2]);
+  const float base = __fmul_rn(__fsub_rn(L, __fmul_rn(2.f, M)), div);
+  const float m2 = __fmul_rn(2.f, M);
+  const float dti = __fmul_rn(k.dt, I);
+  visco_comp<0>(a, k, e, base, m2, M, dti, s1, r1);
+  visco_comp<1>(a, k, e, base, m2, M, dti, s1, r1);
+  visco_comp<2>(a, k, e, base, m2, M, dti, s1, r1);
+  visco_comp<3>(a, k, e, base, m2, M, dti, s1, r1);
+  visco_comp<4>(a, k, e, base, m2, M, dti, s1, r1);
+  visco_comp<5>(a, k, e, base, m2, M, dti, s1, r1);
+}
+
+// ---- generic accessor: global memory ----------------------------------------
+
+struct GlobalAcc {
+  const float* const* tap;  // indexed by logical tap field id
+  const float* const* pnt;  // indexed by logical point id
+  int64_t i, s[3];
+  template <int F, int AX>
+  __device__ __forceinline__ float t(int k) const { return __ldg(tap[F] + i + k * s[AX]); }
+  template <int F>
+  __device__ __forceinline__ float p() const { return __ldg(tap[F] + i); }
+  template <int Q>
+  __device__ __forceinline__ float q() const { return __ldg(pnt[Q] + i); }
+};
+
+struct ElGeneric {
+  const float* tap[NV_];
+  const float* pnt[17];
+  float* out[12];
+  Geom g;
+  ElCoef k;
+};
 
 #define EL_INDEX                                                               \
   const int z = p.g.lo[2] + blockIdx.x * 32 + threadIdx.x;                     \
   const int y = p.g.lo[1] + blockIdx.y * 8 + threadIdx.y;                      \
   const int x = p.g.lo[0] + blockIdx.z;                                        \
   if (z >= p.g.hi[2] || y >= p.g.hi[1]) return;                                \
-  const int64_t sx = p.g.sx, sy = p.g.sy;                                      \
-  const int64_t i = x * sx + y * sy + z;
+  const int64_t i = x * p.g.sx + y * p.g.sy + z;                               \
+  GlobalAcc a{p.tap, p.pnt, i, {p.g.sx, p.g.sy, 1}};
 
-// in = {vx, vy, vz, txx, tyy, tzz, txy, txz, tyz, b}; out = {vx1, vy1, vz1}
 template <int R>
-__global__ void __launch_bounds__(256) el_velocity(ElParams p) {
+__global__ void __launch_bounds__(256) el_velocity(ElGeneric p) {
   EL_INDEX
-  const float *txx = p.in[3], *tyy = p.in[4], *tzz = p.in[5];
-  const float *txy = p.in[6], *txz = p.in[7], *tyz = p.in[8];
-  float bdt = __fmul_rn(p.dt, __ldg(p.in[9] + i));
-  float dvx = __fadd_rn(__fadd_rn(dplus<R>(txx, i, sx, p.c[0]), dminus<R>(txy, i, sy, p.c[1])),
-                        dminus<R>(txz, i, 1, p.c[2]));
-  float dvy = __fadd_rn(__fadd_rn(dminus<R>(txy, i, sx, p.c[0]), dplus<R>(tyy, i, sy, p.c[1])),
-                        dminus<R>(tyz, i, 1, p.c[2]));
-  float dvz = __fadd_rn(__fadd_rn(dminus<R>(txz, i, sx, p.c[0]), dminus<R>(tyz, i, sy, p.c[1])),
-                        dplus<R>(tzz, i, 1, p.c[2]));
-  p.out[0][i] = __fmaf_rn(bdt, dvx, __ldg(p.in[0] + i));
-  p.out[1][i] = __fmaf_rn(bdt, dvy, __ldg(p.in[1] + i));
-  p.out[2][i] = __fmaf_rn(bdt, dvz, __ldg(p.in[2] + i));
+  float o[3];
+  vel_point<R>(a, p.k, o);
+  p.out[0][i] = o[0];
+  p.out[1][i] = o[1];
+  p.out[2][i] = o[2];
 }
 
 template <int R>
-__device__ __forceinline__ void strains(const ElParams& p, int64_t i, int64_t sx, int64_t sy,
-                                        float e[6]) {
-  const float *vx = p.in[0], *vy = p.in[1], *vz = p.in[2];
-  e[0] = dminus<R>(vx, i, sx, p.c[0]);
-  e[1] = dminus<R>(vy, i, sy, p.c[1]);
-  e[2] = dminus<R>(vz, i, 1, p.c[2]);
-  e[3] = __fadd_rn(dplus<R>(vx, i, sy, p.c[1]), dplus<R>(vy, i, sx, p.c[0]));
-  e[4] = __fadd_rn(dplus<R>(vx, i, 1, p.c[2]), dplus<R>(vz, i, sx, p.c[0]));
-  e[5] = __fadd_rn(dplus<R>(vy, i, 1, p.c[2]), dplus<R>(vz, i, sy, p.c[1]));
-}
-
-// in = {vx1, vy1, vz1, txx..tyz (6), lam, mu}; out = {txx1..tyz1}
-template <int R>
-__global__ void __launch_bounds__(256) el_stress(ElParams p) {
+__global__ void __launch_bounds__(256) el_stress(ElGeneric p) {
   EL_INDEX
-  float e[6];
-  strains<R>(p, i, sx, sy, e);
-  const float l = __ldg(p.in[9] + i), mu = __ldg(p.in[10] + i);
-  const float tr = __fadd_rn(__fadd_rn(e[0], e[1]), e[2]);
-  const float ltr = __fmul_rn(l, tr), m2 = __fmul_rn(2.f, mu);
+  float o[6];
+  stress_point<R>(a, p.k, o);
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
-    p.out[c][i] = __fmaf_rn(p.dt, __fmaf_rn(m2, e[c], ltr), __ldg(p.in[3 + c] + i));
-#pragma unroll
-  for (int c = 3; c < 6; ++c)
-    p.out[c][i] = __fmaf_rn(p.dt, __fmul_rn(mu, e[c]), __ldg(p.in[3 + c] + i));
+  for (int c = 0; c < 6; ++c) p.out[c][i] = o[c];
 }
 
-// in = {vx1, vy1, vz1, s(6), r(6), l2m, mus, its} (18 > 16: params packed
-// after r into in[15] region via out-of-line arrays below)
-struct ViscoParams {
-  ElParams e;
-  const float* __restrict__ r0[6];
-  const float* __restrict__ prm[3];
-  float* __restrict__ r1[6];
-};
-
 template <int R>
-__global__ void __launch_bounds__(256) visco_stress(ViscoParams vp) {
-  const ElParams& p = vp.e;
+__global__ void __launch_bounds__(256) visco_stress(ElGeneric p) {
   EL_INDEX
-  float e[6];
-  strains<R>(p, i, sx, sy, e);
-  const float L = __ldg(vp.prm[0] + i), M = __ldg(vp.prm[1] + i), I = __ldg(vp.prm[2] + i);
-  const float div = __fadd_rn(__fadd_rn(e[0], e[1]), e[2]);
-  const float base = __fmul_rn(__fsub_rn(L, __fmul_rn(2.f, M)), div);
-  const float m2 = __fmul_rn(2.f, M);
-  const float dti = __fmul_rn(p.dt, I);
+  float s1[6], r1[6];
+  visco_point<R>(a, p.k, s1, r1);
 #pragma unroll
   for (int c = 0; c < 6; ++c) {
-    float A = c < 3 ? __fmaf_rn(m2, e[c], base) : __fmul_rn(M, e[c]);
-    float r0v = __ldg(vp.r0[c] + i);
-    float rn = __fmaf_rn(-dti, __fadd_rn(r0v, A), r0v);
-    vp.r1[c][i] = rn;
-    p.out[c][i] = __fmaf_rn(p.dt, __fadd_rn(A, rn), __ldg(p.in[3 + c] + i));
+    p.out[c][i] = s1[c];
+    p.out[6 + c][i] = r1[c];
   }
 }
 
-static int fill(ElParams& p, const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
+// ---- stream operators ------------------------------------------------------
+
+// velocity: fronts {txx, txy, txz}; centres {tyy, tzz, txy, txz, tyz};
+// points {vx, vy, vz, b}
+template <int R, int TY, int NF, int NC, int NP>
+struct VelAcc {
+  const StreamCtx<R, TY, NF, NC, NP>& c;
+  template <int F, int AX>
+  __device__ __forceinline__ float t(int k) const {
+    if (AX == 0) return c.xt(F == TXX ? 0 : F == TXY ? 1 : 2, k);
+    constexpr int ci = F == TYY ? 0 : F == TZZ ? 1 : F == TXY ? 2 : F == TXZ ? 3 : 4;
+    return AX == 1 ? c.ct(ci, k, 0) : c.ct(ci, 0, k);
+  }
+  template <int F>
+  __device__ __forceinline__ float p() const { return c.pt(F == VX ? 0 : F == VY ? 1 : F == VZ ? 2 : 3); }
+};
+
+struct VelOp {
+  static constexpr int NF = 3, NC = 5, NP = 4;
+  float* out[3];
+  ElCoef k;
+  template <int R, class Ctx>
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx) const {
+    VelAcc<R, Ctx::L::CY - 2 * R, NF, NC, NP> a{c};
+    float o[3];
+    vel_point<R>(a, k, o);
+    out[0][idx] = o[0];
+    out[1][idx] = o[1];
+    out[2][idx] = o[2];
+  }
+};
+
+// stress: fronts {vx, vy, vz}; centres {vx, vy, vz}; points: s0 (6) +
+// {lam, mu} or + r0 (6) + {l2m, mus, its}
+template <int R, int TY, int NF, int NC, int NP>
+struct StrAcc {
+  const StreamCtx<R, TY, NF, NC, NP>& c;
+  template <int F, int AX>
+  __device__ __forceinline__ float t(int k) const {
+    constexpr int fi = F - VX;
+    return AX == 0 ? c.xt(fi, k) : AX == 1 ? c.ct(fi, k, 0) : c.ct(fi, 0, k);
+  }
+  template <int Q>
+  __device__ __forceinline__ float q() const {
+    // elastic: S0..S0+5 -> 0..5, LAM -> 6, MU -> 7
+    // visco:   S0..5 -> 0..5, R0..R0+5 -> 6..11, L2M/MUS/ITS -> 12..14
+    return c.pt(Q < 6 ? Q : (NP == 8 ? Q - LAM + 6 : (Q < L2M ? Q - R0 + 6 : Q - L2M + 12)));
+  }
+};
+
+struct StressOp {
+  static constexpr int NF = 3, NC = 3, NP = 8;
+  float* out[6];
+  ElCoef k;
+  template <int R, class Ctx>
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx) const {
+    StrAcc<R, Ctx::L::CY - 2 * R, NF, NC, NP> a{c};
+    float o[6];
+    stress_point<R>(a, k, o);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) out[q][idx] = o[q];
+  }
+};
+
+struct ViscoOp {
+  static constexpr int NF = 3, NC = 3, NP = 15;
+  float* out[12];
+  ElCoef k;
+  template <int R, class Ctx>
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx) const {
+    StrAcc<R, Ctx::L::CY - 2 * R, NF, NC, NP> a{c};
+    float s1[6], r1[6];
+    visco_point<R>(a, k, s1, r1);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      out[q][idx] = s1[q];
+      out[6 + q][idx] = r1[q];
+    }
+  }
+};
+
+// ---- host ----------------------------------------------------------------
+
+static int fill(ElGeneric& p, const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
                 int radius, const float* sc, float dt) {
   int rc = make_geom(full, lo, hi, &p.g);
   if (rc) return rc;
@@ -135,14 +273,14 @@ static int fill(ElParams& p, const int64_t full[3], const int64_t lo[3], const i
   for (int a = 0; a < 3; ++a) {
     SDMP_CHECK(lo[a] >= radius && hi[a] + radius <= full[a], "box + radius exceeds FULL");
     for (int k = 0; k < SDMP_MAX_RADIUS; ++k)
-      p.c[a][k] = k < radius ? sc[a * SDMP_MAX_RADIUS + k] : 0.f;
+      p.k.c[a][k] = k < radius ? sc[a * SDMP_MAX_RADIUS + k] : 0.f;
   }
-  p.dt = dt;
+  p.k.dt = dt;
   return SDMP_OK;
 }
 
-template <class P, class K>
-static int launch(const Geom& g, K kernel, const P& params, cudaStream_t st) {
+template <class K>
+static int launch_generic(const Geom& g, K kernel, const ElGeneric& params, cudaStream_t st) {
   dim3 b(32, 8);
   dim3 grid((g.hi[2] - g.lo[2] + 31) / 32, (g.hi[1] - g.lo[1] + 7) / 8, g.hi[0] - g.lo[0]);
   kernel<<<grid, b, 0, st>>>(params);
@@ -150,16 +288,28 @@ static int launch(const Geom& g, K kernel, const P& params, cudaStream_t st) {
   return SDMP_OK;
 }
 
-#define RADIUS_SWITCH(KERNEL, P)                                               \
+// Streaming pays off on thick boxes; thin OWNED slabs take the generic path.
+static bool stream_worth(const Geom& g, int radius) {
+  const int nx = g.hi[0] - g.lo[0], ny = g.hi[1] - g.lo[1];
+  return nx >= 4 * radius && ny >= 16;
+}
+
+static int variant_env() {
+  // 1 forces the generic kernels (tests compare both launch shapes bitwise)
+  const char* e = getenv("SDMP_STAGGERED_VARIANT");
+  return e ? atoi(e) : 0;
+}
+
+#define RADIUS_SWITCH(EXPR_R)                                                  \
   switch (radius) {                                                            \
-    case 1: return launch(P.g, KERNEL<1>, params, st);                         \
-    case 2: return launch(P.g, KERNEL<2>, params, st);                         \
-    case 3: return launch(P.g, KERNEL<3>, params, st);                         \
-    case 4: return launch(P.g, KERNEL<4>, params, st);                         \
-    case 5: return launch(P.g, KERNEL<5>, params, st);                         \
-    case 6: return launch(P.g, KERNEL<6>, params, st);                         \
-    case 7: return launch(P.g, KERNEL<7>, params, st);                         \
-    case 8: return launch(P.g, KERNEL<8>, params, st);                         \
+    case 1: { constexpr int RR = 1; return EXPR_R; }                           \
+    case 2: { constexpr int RR = 2; return EXPR_R; }                           \
+    case 3: { constexpr int RR = 3; return EXPR_R; }                           \
+    case 4: { constexpr int RR = 4; return EXPR_R; }                           \
+    case 5: { constexpr int RR = 5; return EXPR_R; }                           \
+    case 6: { constexpr int RR = 6; return EXPR_R; }                           \
+    case 7: { constexpr int RR = 7; return EXPR_R; }                           \
+    case 8: { constexpr int RR = 8; return EXPR_R; }                           \
   }                                                                            \
   set_error("unsupported radius");                                             \
   return SDMP_EUNSUPPORTED;
@@ -173,16 +323,25 @@ extern "C" int sdmp_elastic_velocity(void* stream, const float* const v0[3],
                                      float* const v1[3], const int64_t full[3],
                                      const int64_t lo[3], const int64_t hi[3], int32_t radius,
                                      const float* sc, float dt) {
-  ElParams params{};
-  int rc = fill(params, full, lo, hi, radius, sc, dt);
+  ElGeneric p{};
+  int rc = fill(p, full, lo, hi, radius, sc, dt);
   if (rc) return rc;
-  if (box_empty(params.g)) return SDMP_OK;
-  for (int c = 0; c < 3; ++c) params.in[c] = v0[c];
-  for (int c = 0; c < 6; ++c) params.in[3 + c] = tau[c];
-  params.in[9] = b;
-  for (int c = 0; c < 3; ++c) params.out[c] = v1[c];
+  if (box_empty(p.g)) return SDMP_OK;
+  for (int c = 0; c < 6; ++c) p.tap[TXX + c] = tau[c];
+  for (int c = 0; c < 3; ++c) p.tap[VX + c] = v0[c];
+  p.tap[PB] = b;
+  for (int c = 0; c < 3; ++c) p.out[c] = v1[c];
   cudaStream_t st = (cudaStream_t)stream;
-  RADIUS_SWITCH(el_velocity, params)
+  const float* arrs[12] = {tau[0], tau[3], tau[4], tau[1], tau[2], tau[3], tau[4], tau[5],
+                           v0[0], v0[1], v0[2], b};
+  if (variant_env() != 1 && stream_worth(p.g, radius) && tma_ok(full, arrs, 12)) {
+    VelOp op{};
+    for (int c = 0; c < 3; ++c) op.out[c] = v1[c];
+    op.k = p.k;
+    RADIUS_SWITCH((RR <= 4 ? launch_stream_op<RR, 16>(op, p.g, full, arrs, st)
+                           : launch_stream_op<RR, 8>(op, p.g, full, arrs, st)))
+  }
+  RADIUS_SWITCH(launch_generic(p.g, el_velocity<RR>, p, st))
 }
 
 extern "C" int sdmp_elastic_stress(void* stream, const float* const v1[3],
@@ -190,17 +349,26 @@ extern "C" int sdmp_elastic_stress(void* stream, const float* const v1[3],
                                    float* const t1[6], const int64_t full[3],
                                    const int64_t lo[3], const int64_t hi[3], int32_t radius,
                                    const float* sc, float dt) {
-  ElParams params{};
-  int rc = fill(params, full, lo, hi, radius, sc, dt);
+  ElGeneric p{};
+  int rc = fill(p, full, lo, hi, radius, sc, dt);
   if (rc) return rc;
-  if (box_empty(params.g)) return SDMP_OK;
-  for (int c = 0; c < 3; ++c) params.in[c] = v1[c];
-  for (int c = 0; c < 6; ++c) params.in[3 + c] = t0[c];
-  params.in[9] = lam;
-  params.in[10] = mu;
-  for (int c = 0; c < 6; ++c) params.out[c] = t1[c];
+  if (box_empty(p.g)) return SDMP_OK;
+  for (int c = 0; c < 3; ++c) p.tap[VX + c] = v1[c];
+  for (int c = 0; c < 6; ++c) p.pnt[S0 + c] = t0[c];
+  p.pnt[LAM] = lam;
+  p.pnt[MU] = mu;
+  for (int c = 0; c < 6; ++c) p.out[c] = t1[c];
   cudaStream_t st = (cudaStream_t)stream;
-  RADIUS_SWITCH(el_stress, params)
+  const float* arrs[14] = {v1[0], v1[1], v1[2], v1[0], v1[1], v1[2],
+                           t0[0], t0[1], t0[2], t0[3], t0[4], t0[5], lam, mu};
+  if (variant_env() != 1 && stream_worth(p.g, radius) && tma_ok(full, arrs, 14)) {
+    StressOp op{};
+    for (int c = 0; c < 6; ++c) op.out[c] = t1[c];
+    op.k = p.k;
+    RADIUS_SWITCH((RR <= 4 ? launch_stream_op<RR, 16>(op, p.g, full, arrs, st)
+                           : launch_stream_op<RR, 8>(op, p.g, full, arrs, st)))
+  }
+  RADIUS_SWITCH(launch_generic(p.g, el_stress<RR>, p, st))
 }
 
 extern "C" int sdmp_visco_stress(void* stream, const float* const v1[3],
@@ -209,18 +377,30 @@ extern "C" int sdmp_visco_stress(void* stream, const float* const v1[3],
                                  float* const r1[6], const int64_t full[3], const int64_t lo[3],
                                  const int64_t hi[3], int32_t radius, const float* sc,
                                  float dt) {
-  ViscoParams params{};
-  int rc = fill(params.e, full, lo, hi, radius, sc, dt);
+  ElGeneric p{};
+  int rc = fill(p, full, lo, hi, radius, sc, dt);
   if (rc) return rc;
-  if (box_empty(params.e.g)) return SDMP_OK;
-  for (int c = 0; c < 3; ++c) params.e.in[c] = v1[c];
+  if (box_empty(p.g)) return SDMP_OK;
+  for (int c = 0; c < 3; ++c) p.tap[VX + c] = v1[c];
   for (int c = 0; c < 6; ++c) {
-    params.e.in[3 + c] = s0[c];
-    params.e.out[c] = s1[c];
-    params.r0[c] = r0[c];
-    params.r1[c] = r1[c];
+    p.pnt[S0 + c] = s0[c];
+    p.pnt[R0 + c] = r0[c];
+    p.out[c] = s1[c];
+    p.out[6 + c] = r1[c];
   }
-  for (int c = 0; c < 3; ++c) params.prm[c] = prm[c];
+  p.pnt[L2M] = prm[0];
+  p.pnt[MUS] = prm[1];
+  p.pnt[ITS] = prm[2];
   cudaStream_t st = (cudaStream_t)stream;
-  RADIUS_SWITCH(visco_stress, params.e)
+  const float* arrs[21] = {v1[0], v1[1], v1[2], v1[0], v1[1], v1[2],
+                           s0[0], s0[1], s0[2], s0[3], s0[4], s0[5],
+                           r0[0], r0[1], r0[2], r0[3], r0[4], r0[5], prm[0], prm[1], prm[2]};
+  if (variant_env() != 1 && stream_worth(p.g, radius) && tma_ok(full, arrs, 21)) {
+    ViscoOp op{};
+    for (int c = 0; c < 12; ++c) op.out[c] = p.out[c];
+    op.k = p.k;
+    RADIUS_SWITCH((RR <= 4 ? launch_stream_op<RR, 16>(op, p.g, full, arrs, st)
+                           : launch_stream_op<RR, 8>(op, p.g, full, arrs, st)))
+  }
+  RADIUS_SWITCH(launch_generic(p.g, visco_stress<RR>, p, st))
 }

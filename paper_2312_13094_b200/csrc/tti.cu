@@ -11,115 +11,201 @@
 //   p1 = 2 p0 - p2 + dt2/m (epsp H0(p) + delp Gzz(r))
 //   r1 = 2 r0 - r2 + dt2/m (delp H0(p) + Gzz(r))
 //
-// Two passes per box: tti_g writes g(p), g(r) on the box grown by R into a
-// FULL-shaped scratch pair; tti_update applies the outer derivative.  The
-// per-point arithmetic is fixed (explicit _rn intrinsics) so CORE/OWNED/
-// DOMAIN launches agree bit for bit.
+// Two passes per box: pass 1 writes g(p), g(r) on the box grown by R into a
+// FULL-shaped scratch pair; pass 2 applies the outer derivative and the
+// update.  Each pass exists as a generic (one thread per point) and a TMA
+// streaming (stream.cuh) launch sharing one per-point routine, so every
+// launch geometry gives identical bits.
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
 
 #include "common.cuh"
+#include "stream.cuh"
 
 namespace sdmp {
 
-struct TTIParams {
-  const float* __restrict__ p0;
-  const float* __restrict__ p2;
-  const float* __restrict__ r0;
-  const float* __restrict__ r2;
-  const float* __restrict__ m;
-  const float* __restrict__ epsp;
-  const float* __restrict__ delp;
-  const float* __restrict__ a[3];
-  float* __restrict__ gp;
-  float* __restrict__ gr;
-  float* __restrict__ p1;
-  float* __restrict__ r1;
-  Geom g;
-  int R;
+struct TTICoef {
   float lap[3][SDMP_NCOEF];
   float d1[3][SDMP_NCOEF];
   float csum0;
   float dt2;
 };
 
-template <int R>
-__device__ __forceinline__ float dcentral(const float* __restrict__ f, int64_t i, int64_t s,
-                                          const float* w) {
-  float acc = __fmul_rn(w[1], __fsub_rn(__ldg(f + i + s), __ldg(f + i - s)));
+// logical ids: tap fields and pointwise fields
+enum { TP = 0, TR, TAX, TAY, TAZ, TGP, TGR, NT_ };
+enum { QP2 = 0, QR0, QR2, QM, QE, QD, QAX, QAY, QAZ, NQ_ };
+
+template <int R, int AX, int F, class A>
+__device__ __forceinline__ float dcentral(const A& a, const float* w) {
+  float acc = __fmul_rn(w[1], __fsub_rn(a.template t<F, AX>(1), a.template t<F, AX>(-1)));
 #pragma unroll
   for (int k = 2; k <= R; ++k)
-    acc = __fmaf_rn(w[k], __fsub_rn(__ldg(f + i + k * s), __ldg(f + i - k * s)), acc);
+    acc = __fmaf_rn(w[k], __fsub_rn(a.template t<F, AX>(k), a.template t<F, AX>(-k)), acc);
   return acc;
 }
 
-template <int R>
-__global__ void __launch_bounds__(256) tti_g(TTIParams p, int glo0, int glo1, int glo2,
-                                             int ghi0, int ghi1, int ghi2) {
-  const int z = glo2 + blockIdx.x * 32 + threadIdx.x;
-  const int y = glo1 + blockIdx.y * 8 + threadIdx.y;
-  const int x = glo0 + blockIdx.z;
-  if (z >= ghi2 || y >= ghi1 || x >= ghi0) return;
-  const int64_t s[3] = {p.g.sx, p.g.sy, 1};
-  const int64_t i = x * s[0] + y * s[1] + z;
-  float ax = __ldg(p.a[0] + i), ay = __ldg(p.a[1] + i), az = __ldg(p.a[2] + i);
-  float gpv = __fmul_rn(ax, dcentral<R>(p.p0, i, s[0], p.d1[0]));
-  gpv = __fmaf_rn(ay, dcentral<R>(p.p0, i, s[1], p.d1[1]), gpv);
-  gpv = __fmaf_rn(az, dcentral<R>(p.p0, i, s[2], p.d1[2]), gpv);
-  float grv = __fmul_rn(ax, dcentral<R>(p.r0, i, s[0], p.d1[0]));
-  grv = __fmaf_rn(ay, dcentral<R>(p.r0, i, s[1], p.d1[1]), grv);
-  grv = __fmaf_rn(az, dcentral<R>(p.r0, i, s[2], p.d1[2]), grv);
-  p.gp[i] = gpv;
-  p.gr[i] = grv;
-}
-
-template <int R>
-__device__ __forceinline__ float outer(const float* __restrict__ a, const float* __restrict__ g,
-                                       int64_t i, int64_t s, const float* w) {
+// D_AX (a_AX g) with a, g both tapped
+template <int R, int AX, int FA, int FG, class A>
+__device__ __forceinline__ float outer(const A& a, const float* w) {
   float acc = 0.f;
 #pragma unroll
   for (int k = 1; k <= R; ++k) {
-    float hi = __fmul_rn(__ldg(a + i + k * s), g[i + k * s]);
-    float lo = __fmul_rn(__ldg(a + i - k * s), g[i - k * s]);
+    const float hi = __fmul_rn(a.template t<FA, AX>(k), a.template t<FG, AX>(k));
+    const float lo = __fmul_rn(a.template t<FA, AX>(-k), a.template t<FG, AX>(-k));
     acc = k == 1 ? __fmul_rn(w[1], __fsub_rn(hi, lo)) : __fmaf_rn(w[k], __fsub_rn(hi, lo), acc);
   }
   return acc;
 }
 
+template <int R, class A>
+__device__ __forceinline__ void g_point(const A& a, const TTICoef& c, float& gp, float& gr) {
+  const float ax = a.template q<QAX>(), ay = a.template q<QAY>(), az = a.template q<QAZ>();
+  gp = __fmul_rn(ax, dcentral<R, 0, TP>(a, c.d1[0]));
+  gp = __fmaf_rn(ay, dcentral<R, 1, TP>(a, c.d1[1]), gp);
+  gp = __fmaf_rn(az, dcentral<R, 2, TP>(a, c.d1[2]), gp);
+  gr = __fmul_rn(ax, dcentral<R, 0, TR>(a, c.d1[0]));
+  gr = __fmaf_rn(ay, dcentral<R, 1, TR>(a, c.d1[1]), gr);
+  gr = __fmaf_rn(az, dcentral<R, 2, TR>(a, c.d1[2]), gr);
+}
+
+template <int R, class A>
+__device__ __forceinline__ void u_point(const A& a, const TTICoef& c, float& p1, float& r1) {
+  float gzp = outer<R, 0, TAX, TGP>(a, c.d1[0]);
+  gzp = __fadd_rn(gzp, outer<R, 1, TAY, TGP>(a, c.d1[1]));
+  gzp = __fadd_rn(gzp, outer<R, 2, TAZ, TGP>(a, c.d1[2]));
+  float gzr = outer<R, 0, TAX, TGR>(a, c.d1[0]);
+  gzr = __fadd_rn(gzr, outer<R, 1, TAY, TGR>(a, c.d1[1]));
+  gzr = __fadd_rn(gzr, outer<R, 2, TAZ, TGR>(a, c.d1[2]));
+  const float c0 = a.template t<TP, 0>(0);
+  float lap = __fmul_rn(c.csum0, c0);
+#pragma unroll
+  for (int k = 1; k <= R; ++k)
+    lap = __fmaf_rn(c.lap[0][k], __fadd_rn(a.template t<TP, 0>(-k), a.template t<TP, 0>(k)), lap);
+#pragma unroll
+  for (int k = 1; k <= R; ++k)
+    lap = __fmaf_rn(c.lap[1][k], __fadd_rn(a.template t<TP, 1>(-k), a.template t<TP, 1>(k)), lap);
+#pragma unroll
+  for (int k = 1; k <= R; ++k)
+    lap = __fmaf_rn(c.lap[2][k], __fadd_rn(a.template t<TP, 2>(-k), a.template t<TP, 2>(k)), lap);
+  const float h0 = __fsub_rn(lap, gzp);
+  const float sc = __fdiv_rn(c.dt2, a.template q<QM>());
+  const float e = a.template q<QE>(), d = a.template q<QD>();
+  const float pp = __fmaf_rn(d, gzr, __fmul_rn(e, h0));
+  const float rr = __fmaf_rn(d, h0, gzr);
+  const float pt = __fsub_rn(__fmul_rn(2.f, c0), a.template q<QP2>());
+  const float r0v = a.template q<QR0>();
+  const float rt = __fsub_rn(__fmul_rn(2.f, r0v), a.template q<QR2>());
+  p1 = __fmaf_rn(sc, pp, pt);
+  r1 = __fmaf_rn(sc, rr, rt);
+}
+
+// ---- generic launch ---------------------------------------------------------
+
+struct TTIGlobalAcc {
+  const float* const* tap;
+  const float* const* pnt;
+  int64_t i, s[3];
+  template <int F, int AX>
+  __device__ __forceinline__ float t(int k) const { return __ldg(tap[F] + i + k * s[AX]); }
+  template <int Q>
+  __device__ __forceinline__ float q() const { return __ldg(pnt[Q] + i); }
+};
+
+struct TTIGeneric {
+  const float* tap[NT_];
+  const float* pnt[NQ_];
+  float* out[2];
+  Geom g;
+  TTICoef c;
+};
+
 template <int R>
-__global__ void __launch_bounds__(256) tti_update(TTIParams p) {
+__global__ void __launch_bounds__(256) tti_g(TTIGeneric p) {
   const int z = p.g.lo[2] + blockIdx.x * 32 + threadIdx.x;
   const int y = p.g.lo[1] + blockIdx.y * 8 + threadIdx.y;
   const int x = p.g.lo[0] + blockIdx.z;
   if (z >= p.g.hi[2] || y >= p.g.hi[1]) return;
-  const int64_t s[3] = {p.g.sx, p.g.sy, 1};
-  const int64_t i = x * s[0] + y * s[1] + z;
-  float gzp = outer<R>(p.a[0], p.gp, i, s[0], p.d1[0]);
-  gzp = __fadd_rn(gzp, outer<R>(p.a[1], p.gp, i, s[1], p.d1[1]));
-  gzp = __fadd_rn(gzp, outer<R>(p.a[2], p.gp, i, s[2], p.d1[2]));
-  float gzr = outer<R>(p.a[0], p.gr, i, s[0], p.d1[0]);
-  gzr = __fadd_rn(gzr, outer<R>(p.a[1], p.gr, i, s[1], p.d1[1]));
-  gzr = __fadd_rn(gzr, outer<R>(p.a[2], p.gr, i, s[2], p.d1[2]));
-  const float* __restrict__ u = p.p0;
-  float c0 = __ldg(u + i);
-  float lap = __fmul_rn(p.csum0, c0);
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int k = 1; k <= R; ++k)
-      lap = __fmaf_rn(p.lap[a][k], __fadd_rn(__ldg(u + i - k * s[a]), __ldg(u + i + k * s[a])), lap);
-  float h0 = __fsub_rn(lap, gzp);
-  float sc = __fdiv_rn(p.dt2, __ldg(p.m + i));
-  float e = __ldg(p.epsp + i), d = __ldg(p.delp + i);
-  float pp = __fmaf_rn(d, gzr, __fmul_rn(e, h0));
-  float rr = __fmaf_rn(d, h0, gzr);
-  float pt = __fsub_rn(__fmul_rn(2.f, c0), __ldg(p.p2 + i));
-  float r0v = __ldg(p.r0 + i);
-  float rt = __fsub_rn(__fmul_rn(2.f, r0v), __ldg(p.r2 + i));
-  p.p1[i] = __fmaf_rn(sc, pp, pt);
-  p.r1[i] = __fmaf_rn(sc, rr, rt);
+  const int64_t i = x * p.g.sx + y * p.g.sy + z;
+  TTIGlobalAcc a{p.tap, p.pnt, i, {p.g.sx, p.g.sy, 1}};
+  float gp, gr;
+  g_point<R>(a, p.c, gp, gr);
+  p.out[0][i] = gp;
+  p.out[1][i] = gr;
 }
+
+template <int R>
+__global__ void __launch_bounds__(256) tti_update(TTIGeneric p) {
+  const int z = p.g.lo[2] + blockIdx.x * 32 + threadIdx.x;
+  const int y = p.g.lo[1] + blockIdx.y * 8 + threadIdx.y;
+  const int x = p.g.lo[0] + blockIdx.z;
+  if (z >= p.g.hi[2] || y >= p.g.hi[1]) return;
+  const int64_t i = x * p.g.sx + y * p.g.sy + z;
+  TTIGlobalAcc a{p.tap, p.pnt, i, {p.g.sx, p.g.sy, 1}};
+  float p1, r1;
+  u_point<R>(a, p.c, p1, r1);
+  p.out[0][i] = p1;
+  p.out[1][i] = r1;
+}
+
+// ---- stream operators --------------------------------------------------------
+
+// pass 1: fronts {p, r}; centres {p, r}; points {ax, ay, az}
+template <int R, int TY, int NF, int NC, int NP>
+struct GAcc {
+  const StreamCtx<R, TY, NF, NC, NP>& c;
+  template <int F, int AX>
+  __device__ __forceinline__ float t(int k) const {
+    constexpr int fi = F == TP ? 0 : 1;
+    return AX == 0 ? c.xt(fi, k) : AX == 1 ? c.ct(fi, k, 0) : c.ct(fi, 0, k);
+  }
+  template <int Q>
+  __device__ __forceinline__ float q() const { return c.pt(Q - QAX); }
+};
+
+struct GOp {
+  static constexpr int NF = 2, NC = 2, NP = 3;
+  float* out[2];
+  TTICoef k;
+  template <int R, class Ctx>
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx) const {
+    GAcc<R, Ctx::L::CY - 2 * R, NF, NC, NP> a{c};
+    float gp, gr;
+    g_point<R>(a, k, gp, gr);
+    out[0][idx] = gp;
+    out[1][idx] = gr;
+  }
+};
+
+// pass 2: fronts {ax, gp, gr, p}; centres {ay, az, gp, gr, p};
+// points {p2, r0, r2, m, epsp, delp}
+template <int R, int TY, int NF, int NC, int NP>
+struct UAcc {
+  const StreamCtx<R, TY, NF, NC, NP>& c;
+  template <int F, int AX>
+  __device__ __forceinline__ float t(int k) const {
+    if (AX == 0) return c.xt(F == TAX ? 0 : F == TGP ? 1 : F == TGR ? 2 : 3, k);
+    constexpr int ci = F == TAY ? 0 : F == TAZ ? 1 : F == TGP ? 2 : F == TGR ? 3 : 4;
+    return AX == 1 ? c.ct(ci, k, 0) : c.ct(ci, 0, k);
+  }
+  template <int Q>
+  __device__ __forceinline__ float q() const { return c.pt(Q); }
+};
+
+struct UOp {
+  static constexpr int NF = 4, NC = 5, NP = 6;
+  float* out[2];
+  TTICoef k;
+  template <int R, class Ctx>
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx) const {
+    UAcc<R, Ctx::L::CY - 2 * R, NF, NC, NP> a{c};
+    float p1, r1;
+    u_point<R>(a, k, p1, r1);
+    out[0][idx] = p1;
+    out[1][idx] = r1;
+  }
+};
 
 // FULL-shaped scratch pair per (device, size), grow-only, never freed
 // before process exit (the plan reuses it every step).
@@ -134,24 +220,58 @@ static std::pair<float*, float*> scratch(int64_t n) {
   if (it != cache.end()) return it->second;
   float *a = nullptr, *b = nullptr;
   if (cudaMalloc(&a, n * sizeof(float)) != cudaSuccess) return {nullptr, nullptr};
-  if (cudaMalloc(&b, n * sizeof(float)) != cudaSuccess) { cudaFree(a); return {nullptr, nullptr}; }
+  if (cudaMalloc(&b, n * sizeof(float)) != cudaSuccess) {
+    cudaFree(a);
+    return {nullptr, nullptr};
+  }
   cudaMemset(a, 0, n * sizeof(float));
   cudaMemset(b, 0, n * sizeof(float));
   cache[key] = {a, b};
   return {a, b};
 }
 
-// R = first-derivative radius (SO/2); the nested operator reaches 2R.
+static int variant_env() {
+  // 1 forces the generic kernels (tests compare both launch shapes bitwise)
+  const char* e = getenv("SDMP_TTI_VARIANT");
+  return e ? atoi(e) : 0;
+}
+
 template <int R>
-static int launch(TTIParams& p, cudaStream_t st) {
-  int glo[3], ghi[3];
+static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3]) {
+  // pass 1 on the box grown by R (g is read up to R away by pass 2)
+  TTIGeneric p1 = p;
   for (int a = 0; a < 3; ++a) {
-    glo[a] = p.g.lo[a] - R;
-    ghi[a] = p.g.hi[a] + R;
+    p1.g.lo[a] = p.g.lo[a] - R;
+    p1.g.hi[a] = p.g.hi[a] + R;
   }
+  p1.out[0] = const_cast<float*>(p.tap[TGP]);
+  p1.out[1] = const_cast<float*>(p.tap[TGR]);
+  const float* a1[7] = {p.tap[TP], p.tap[TR], p.tap[TP], p.tap[TR], p.pnt[QAX], p.pnt[QAY],
+                        p.pnt[QAZ]};
+  const float* a2[15] = {p.tap[TAX], p.tap[TGP], p.tap[TGR], p.tap[TP],
+                         p.tap[TAY], p.tap[TAZ], p.tap[TGP], p.tap[TGR], p.tap[TP],
+                         p.pnt[QP2], p.pnt[QR0], p.pnt[QR2], p.pnt[QM], p.pnt[QE], p.pnt[QD]};
+  const bool thick = (p.g.hi[0] - p.g.lo[0]) >= 4 * R && (p.g.hi[1] - p.g.lo[1]) >= 16;
+  const bool stream = variant_env() != 1 && thick && tma_ok(full, a1, 7) && tma_ok(full, a2, 15);
   dim3 b(32, 8);
-  dim3 g1((ghi[2] - glo[2] + 31) / 32, (ghi[1] - glo[1] + 7) / 8, ghi[0] - glo[0]);
-  tti_g<R><<<g1, b, 0, st>>>(p, glo[0], glo[1], glo[2], ghi[0], ghi[1], ghi[2]);
+  if (stream) {
+    GOp g{};
+    g.out[0] = p1.out[0];
+    g.out[1] = p1.out[1];
+    g.k = p.c;
+    int rc = R <= 4 ? launch_stream_op<R, 16>(g, p1.g, full, a1, st)
+                    : launch_stream_op<R, 8>(g, p1.g, full, a1, st);
+    if (rc) return rc;
+    UOp u{};
+    u.out[0] = p.out[0];
+    u.out[1] = p.out[1];
+    u.k = p.c;
+    return R <= 4 ? launch_stream_op<R, 16>(u, p.g, full, a2, st)
+                  : launch_stream_op<R, 8>(u, p.g, full, a2, st);
+  }
+  dim3 g1((p1.g.hi[2] - p1.g.lo[2] + 31) / 32, (p1.g.hi[1] - p1.g.lo[1] + 7) / 8,
+          p1.g.hi[0] - p1.g.lo[0]);
+  tti_g<R><<<g1, b, 0, st>>>(p1);
   SDMP_LAUNCHED();
   dim3 g2((p.g.hi[2] - p.g.lo[2] + 31) / 32, (p.g.hi[1] - p.g.lo[1] + 7) / 8,
           p.g.hi[0] - p.g.lo[0]);
@@ -163,7 +283,7 @@ static int launch(TTIParams& p, cudaStream_t st) {
 int tti_update_entry(cudaStream_t st, const float* const in[10], float* p1, float* r1,
                      const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
                      int32_t radius, const float* lap_c, const float* d1_c, float dt2) {
-  TTIParams p;
+  TTIGeneric p{};
   int rc = make_geom(full, lo, hi, &p.g);
   if (rc) return rc;
   if (box_empty(p.g)) return SDMP_OK;
@@ -172,36 +292,39 @@ int tti_update_entry(cudaStream_t st, const float* const in[10], float* p1, floa
   for (int a = 0; a < 3; ++a)
     SDMP_CHECK(lo[a] >= 2 * radius && hi[a] + 2 * radius <= full[a],
                "tti box + 2*radius exceeds FULL (halo must be >= SO)");
-  p.p0 = in[0]; p.p2 = in[1]; p.r0 = in[2]; p.r2 = in[3]; p.m = in[4];
-  p.epsp = in[5]; p.delp = in[6]; p.a[0] = in[7]; p.a[1] = in[8]; p.a[2] = in[9];
-  p.p1 = p1; p.r1 = r1;
-  p.R = radius;
-  float cs = 0.f;
-  for (int a = 0; a < 3; ++a) {
-    for (int k = 0; k < SDMP_NCOEF; ++k) {
-      p.lap[a][k] = k <= radius ? lap_c[a * SDMP_NCOEF + k] : 0.f;
-      p.d1[a][k] = (k >= 1 && k <= radius) ? d1_c[a * SDMP_NCOEF + k] : 0.f;
-    }
-    cs = cs + p.lap[a][0];
-  }
-  p.csum0 = cs;
-  p.dt2 = dt2;
   auto sc = scratch(full[0] * full[1] * full[2]);
   if (!sc.first) {
     set_error("tti: scratch allocation failed");
     return SDMP_ECUDA;
   }
-  p.gp = sc.first;
-  p.gr = sc.second;
+  // in = {p0, p2, r0, r2, m, epsp, delp, ax, ay, az}
+  p.tap[TP] = in[0]; p.tap[TR] = in[2];
+  p.tap[TAX] = in[7]; p.tap[TAY] = in[8]; p.tap[TAZ] = in[9];
+  p.tap[TGP] = sc.first; p.tap[TGR] = sc.second;
+  p.pnt[QP2] = in[1]; p.pnt[QR0] = in[2]; p.pnt[QR2] = in[3]; p.pnt[QM] = in[4];
+  p.pnt[QE] = in[5]; p.pnt[QD] = in[6];
+  p.pnt[QAX] = in[7]; p.pnt[QAY] = in[8]; p.pnt[QAZ] = in[9];
+  p.out[0] = p1;
+  p.out[1] = r1;
+  float cs = 0.f;
+  for (int a = 0; a < 3; ++a) {
+    for (int k = 0; k < SDMP_NCOEF; ++k) {
+      p.c.lap[a][k] = k <= radius ? lap_c[a * SDMP_NCOEF + k] : 0.f;
+      p.c.d1[a][k] = (k >= 1 && k <= radius) ? d1_c[a * SDMP_NCOEF + k] : 0.f;
+    }
+    cs = cs + p.c.lap[a][0];
+  }
+  p.c.csum0 = cs;
+  p.c.dt2 = dt2;
   switch (radius) {
-    case 1: return launch<1>(p, st);
-    case 2: return launch<2>(p, st);
-    case 3: return launch<3>(p, st);
-    case 4: return launch<4>(p, st);
-    case 5: return launch<5>(p, st);
-    case 6: return launch<6>(p, st);
-    case 7: return launch<7>(p, st);
-    case 8: return launch<8>(p, st);
+    case 1: return launch<1>(p, st, full);
+    case 2: return launch<2>(p, st, full);
+    case 3: return launch<3>(p, st, full);
+    case 4: return launch<4>(p, st, full);
+    case 5: return launch<5>(p, st, full);
+    case 6: return launch<6>(p, st, full);
+    case 7: return launch<7>(p, st, full);
+    case 8: return launch<8>(p, st, full);
   }
   set_error("tti: unsupported radius");
   return SDMP_EUNSUPPORTED;
