@@ -232,7 +232,15 @@ class Function:
             raise ValueError(f"a field named {name!r} with the same spec already exists")
         _FUNCS[self.spec] = self
         nd = grid.ndims
-        self.halo3 = tuple(self.spec.halo) + (0,) * (3 - nd)
+        # device layout: halo per side = FieldSpec.halo, except that the z
+        # halo of 3D fields is padded up to a multiple of 8 (the paper's
+        # "padding" region): keeps rows 32 B-aligned for TMA and
+        # every TMA box start non-negative.  Padding is zero like the exterior
+        # halo; exchange radii and all DOMAIN-relative boxes are unchanged.
+        h = tuple(self.spec.halo)
+        if nd == 3:
+            h = h[:2] + ((h[2] + 7) // 8 * 8,)
+        self.halo3 = h + (0,) * (3 - nd)
         loc = tuple(grid.local_shape) + (1,) * (3 - nd)
         self.local3 = loc
         self.full3 = tuple(n + 2 * h for n, h in zip(loc, self.halo3))

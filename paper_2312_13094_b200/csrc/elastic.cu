@@ -334,7 +334,8 @@ extern "C" int sdmp_elastic_velocity(void* stream, const float* const v0[3],
   cudaStream_t st = (cudaStream_t)stream;
   const float* arrs[12] = {tau[0], tau[3], tau[4], tau[1], tau[2], tau[3], tau[4], tau[5],
                            v0[0], v0[1], v0[2], b};
-  if (variant_env() != 1 && stream_worth(p.g, radius) && tma_ok(full, arrs, 12)) {
+  if (variant_env() != 1 && stream_worth(p.g, radius) && stream_fits(p.g, radius) &&
+      tma_ok(full, arrs, 12)) {
     VelOp op{};
     for (int c = 0; c < 3; ++c) op.out[c] = v1[c];
     op.k = p.k;
@@ -361,7 +362,8 @@ extern "C" int sdmp_elastic_stress(void* stream, const float* const v1[3],
   cudaStream_t st = (cudaStream_t)stream;
   const float* arrs[14] = {v1[0], v1[1], v1[2], v1[0], v1[1], v1[2],
                            t0[0], t0[1], t0[2], t0[3], t0[4], t0[5], lam, mu};
-  if (variant_env() != 1 && stream_worth(p.g, radius) && tma_ok(full, arrs, 14)) {
+  if (variant_env() != 1 && stream_worth(p.g, radius) && stream_fits(p.g, radius) &&
+      tma_ok(full, arrs, 14)) {
     StressOp op{};
     for (int c = 0; c < 6; ++c) op.out[c] = t1[c];
     op.k = p.k;
@@ -395,7 +397,8 @@ extern "C" int sdmp_visco_stress(void* stream, const float* const v1[3],
   const float* arrs[21] = {v1[0], v1[1], v1[2], v1[0], v1[1], v1[2],
                            s0[0], s0[1], s0[2], s0[3], s0[4], s0[5],
                            r0[0], r0[1], r0[2], r0[3], r0[4], r0[5], prm[0], prm[1], prm[2]};
-  if (variant_env() != 1 && stream_worth(p.g, radius) && tma_ok(full, arrs, 21)) {
+  if (variant_env() != 1 && stream_worth(p.g, radius) && stream_fits(p.g, radius) &&
+      tma_ok(full, arrs, 21)) {
     ViscoOp op{};
     for (int c = 0; c < 12; ++c) op.out[c] = p.out[c];
     op.k = p.k;

@@ -460,7 +460,7 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
   p.A = A; p.B = B; p.C = C;
 
   const int R = radius[0];
-  const bool streamable = radius[1] == R && radius[2] == R && R >= 1 &&
+  const bool streamable = radius[1] == R && radius[2] == R && R >= 1 && lo[2] >= round4(R) &&
                           (full[2] % 4 == 0) && (lo[2] % 4 == 0) && ((hi[2] - lo[2]) % 4 == 0) &&
                           (((uintptr_t)u0 | (uintptr_t)u1 | (uintptr_t)u2 | (uintptr_t)m) % 16 == 0);
   // unaligned / unequal-radius boxes always take the generic kernel

@@ -20,6 +20,9 @@
 // generic kernels through accessor templates (bit-identical results).
 #pragma once
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "tma.cuh"
 
 namespace sdmp {
@@ -90,7 +93,9 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
     fence_barrier_init();
   }
   __syncthreads();
-  const int z0 = g.lo[2] + blockIdx.x * kSZ;
+  // TMA boxes must start on a 16 B boundary along z: tiles are aligned down
+  // to a multiple of 4 floats and lanes left of the box are masked off.
+  const int z0 = (g.lo[2] & ~3) + blockIdx.x * kSZ;
   const int y0 = g.lo[1] + blockIdx.y * TY;
   const int xa = g.lo[0] + blockIdx.z * xchunk;
   const int xb = min(xa + xchunk, g.hi[0]);
@@ -125,7 +130,7 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
   }
 
   const int z = z0 + lane, y = y0 + warp;
-  const bool active = (z < g.hi[2]) && (y < g.hi[1]);
+  const bool active = (z >= g.lo[2]) && (z < g.hi[2]) && (y < g.hi[1]);
   float w[NF > 0 ? NF : 1][2 * R + 1];
 #pragma unroll
   for (int f = 0; f < NF; ++f)
@@ -200,15 +205,36 @@ int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const f
     if (rc) return rc;
   }
   const int nz = g.hi[2] - g.lo[2], ny = g.hi[1] - g.lo[1], nx = g.hi[0] - g.lo[0];
-  const int tz = (nz + kSZ - 1) / kSZ, ty = (ny + TY - 1) / TY;
+  const int tz = (nz + (g.lo[2] & 3) + kSZ - 1) / kSZ, ty = (ny + TY - 1) / TY;
   int nch = stream_chunks((int64_t)tz * ty, nx, R);
   const int chunk = (nx + nch - 1) / nch;
   nch = (nx + chunk - 1) / chunk;
   SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");
   dim3 grid(tz, ty, nch), block(32, TY + 1);
+  const bool dbg = getenv("SDMP_DEBUG") != nullptr;
+  if (dbg)
+    fprintf(stderr,
+            "[sdmp] stream_kernel R=%d TY=%d NF=%d NC=%d NP=%d box=[%d,%d,%d]-[%d,%d,%d] "
+            "full=[%ld,%ld,%ld] grid=(%d,%d,%d) chunk=%d smem=%d S=%d stage=%d\n",
+            R, TY, Op::NF, Op::NC, Op::NP, g.lo[0], g.lo[1], g.lo[2], g.hi[0], g.hi[1], g.hi[2],
+            (long)full[0], (long)full[1], (long)full[2], tz, ty, nch, chunk, L::BYTES, L::S,
+            L::STAGE);
   stream_kernel<R, TY, Op><<<grid, block, L::BYTES, st>>>(maps, op, g, chunk);
   SDMP_LAUNCHED();
+  if (dbg) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    fprintf(stderr, "[sdmp]   -> %s\n", cudaGetErrorString(e));
+  }
   return SDMP_OK;
+}
+
+// TMA tile loads must start on a 16 B boundary along the innermost (z)
+// axis: on sm_100a / driver 580 a misaligned box start raises "illegal
+// instruction" (the engine aligns tiles down to 4 floats).  Loads start at
+// (z0 - round4(R), y0 - R, x0 - R); boxes whose loads would start below 0
+// take the generic kernel.
+inline bool stream_fits(const Geom& g, int R) {
+  return (g.lo[2] & ~3) - sround4(R) >= 0 && g.lo[1] - R >= 0 && g.lo[0] - R >= 0;
 }
 
 // TMA-eligibility of a set of arrays: 16 B-aligned bases, FULL z multiple of 4.

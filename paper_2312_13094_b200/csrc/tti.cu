@@ -252,7 +252,8 @@ static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3]) {
                          p.tap[TAY], p.tap[TAZ], p.tap[TGP], p.tap[TGR], p.tap[TP],
                          p.pnt[QP2], p.pnt[QR0], p.pnt[QR2], p.pnt[QM], p.pnt[QE], p.pnt[QD]};
   const bool thick = (p.g.hi[0] - p.g.lo[0]) >= 4 * R && (p.g.hi[1] - p.g.lo[1]) >= 16;
-  const bool stream = variant_env() != 1 && thick && tma_ok(full, a1, 7) && tma_ok(full, a2, 15);
+  const bool stream = variant_env() != 1 && thick && stream_fits(p1.g, R) && stream_fits(p.g, R) &&
+                      tma_ok(full, a1, 7) && tma_ok(full, a2, 15);
   dim3 b(32, 8);
   if (stream) {
     GOp g{};
