@@ -36,12 +36,16 @@ int star_update(cudaStream_t, const float*, const float*, const float*, float*, 
 int tti_update_entry(cudaStream_t, const float* const*, float*, float*, const int64_t*,
                      const int64_t*, const int64_t*, int32_t, const float*, const float*, float);
 int inject(cudaStream_t, float*, const int64_t*, const int32_t*, int, const int32_t*,
-           const float*, const float*, float, const float*);
-int interpolate(cudaStream_t, const float*, const int64_t*, const float*, int, int, float*);
+           const float*, const float*, float, const float*, const int64_t*, int64_t, int64_t);
+int interpolate(cudaStream_t, const float*, const int64_t*, const float*, int, int, float*,
+                const int64_t*, int64_t, int64_t);
+int set_ctr(cudaStream_t, int64_t*, int64_t, int64_t);
+int tick_ctr(cudaStream_t, int64_t*);
 int copy_box(cudaStream_t, const float*, const int64_t*, const int64_t*, float*, const int64_t*,
              const int64_t*, const int64_t*, int);
-int signal_flags(cudaStream_t, uint32_t* const*, int, uint32_t);
-int wait_flags(cudaStream_t, uint32_t* const*, int, uint32_t, unsigned long long, int*);
+int signal_flags(cudaStream_t, uint32_t* const*, int, uint32_t, const int64_t*, int, int);
+int wait_flags(cudaStream_t, uint32_t* const*, int, uint32_t, unsigned long long, int*,
+               const int64_t*, int, int);
 
 }  // namespace sdmp
 
@@ -93,12 +97,23 @@ struct sdmp_plan {
   cudaEvent_t ev_step = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_user[32];
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  // copy-engine fan-out for halo posts: messages round-robin over kCopy
+  // streams so several copy engines move faces/edges concurrently
+  static constexpr int kCopy = 4;
+  cudaStream_t cs[kCopy] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_cdone[kCopy] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<Field> fields;
   std::vector<uint32_t*> flags;  // peer flag arrays
   uint32_t* local_flags = nullptr;
   std::vector<SparseSet> sparse;
   std::vector<Action> actions;
   int64_t steps_done = 0;
+  // device step counter {time, steps_done}: sparse rows and exchange epochs
+  // are read from it so a captured period of steps can be replayed
+  int64_t* dev_ctr = nullptr;
+  bool graph_on = false;
+  int period = 1;
+  std::map<int64_t, cudaGraphExec_t> graphs;  // by time % period
   int* err_host = nullptr;
   int* err_dev = nullptr;
   int64_t timeout_ms = 30000;
@@ -206,37 +221,48 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       float* fld = resolve(p, I[2], I[3], time);
       const float* m = resolve(p, I[4], 0, time);
       const SparseSet& ss = p->sparse[I[5]];
-      int64_t row = time - ss.t0;
-      if (row < 0) return SDMP_OK;
-      return inject(st, fld, ss.node, ss.ptr, ss.nnodes, ss.pid, ss.w,
-                    ss.series + row * ss.stride, F[0], m);
+      if (time < ss.t0) return SDMP_OK;
+      return inject(st, fld, ss.node, ss.ptr, ss.nnodes, ss.pid, ss.w, ss.series, F[0], m,
+                    p->dev_ctr, ss.stride, ss.t0);
     }
     case SDMP_ACT_INTERP: {
       const float* fld = resolve(p, I[2], I[3], time);
       const SparseSet& ss = p->sparse[I[4]];
-      int64_t row = time - ss.t0;
-      if (row < 0) return SDMP_OK;
-      return interpolate(st, fld, ss.node, ss.w, ss.npts, ss.ncorner,
-                         ss.series + row * ss.stride);
+      if (time < ss.t0) return SDMP_OK;
+      return interpolate(st, fld, ss.node, ss.w, ss.npts, ss.ncorner, ss.series, p->dev_ctr,
+                         ss.stride, ss.t0);
     }
     case SDMP_ACT_POST: {
       // [k,s, phase, nmsg, engine, msgs(12 each: fsrc,t,fdst,slo3,dlo3,ext3)..., nsig, (flags_id, slot)...]
       const int64_t phase = I[2], nmsg = I[3];
       const int engine = (int)I[4];
       const int64_t* m = I + 5;
+      const int fan = (engine == 0 && nmsg > 1) ? (int)(nmsg < sdmp_plan::kCopy ? nmsg
+                                                                              : sdmp_plan::kCopy)
+                                                : 1;
+      if (fan > 1) {
+        SDMP_CUDA(cudaEventRecord(p->ev_fork, st));
+        for (int c = 0; c < fan; ++c) SDMP_CUDA(cudaStreamWaitEvent(p->cs[c], p->ev_fork, 0));
+      }
       for (int64_t q = 0; q < nmsg; ++q, m += 12) {
         const float* src = resolve(p, m[0], m[1], time);
         float* dst = resolve(p, m[2], m[1], time);
-        int rc = copy_box(st, src, p->fields[m[0]].full, m + 3, dst, p->fields[m[2]].full,
+        cudaStream_t cst = fan > 1 ? p->cs[q % fan] : st;
+        int rc = copy_box(cst, src, p->fields[m[0]].full, m + 3, dst, p->fields[m[2]].full,
                           m + 6, m + 9, engine);
         if (rc) return rc;
+      }
+      if (fan > 1) {
+        for (int c = 0; c < fan; ++c) {
+          SDMP_CUDA(cudaEventRecord(p->ev_cdone[c], p->cs[c]));
+          SDMP_CUDA(cudaStreamWaitEvent(st, p->ev_cdone[c], 0));
+        }
       }
       const int64_t nsig = *m++;
       uint32_t* ptrs[32];
       SDMP_CHECK(nsig <= 32, "too many signals");
       for (int64_t q = 0; q < nsig; ++q) ptrs[q] = p->flags[m[2 * q]] + m[2 * q + 1];
-      const uint32_t epoch = (uint32_t)(p->steps_done * p->phases + phase + 1);
-      return signal_flags(st, ptrs, (int)nsig, epoch);
+      return signal_flags(st, ptrs, (int)nsig, 0, p->dev_ctr, p->phases, (int)phase);
     }
     case SDMP_ACT_WAIT: {
       // [k,s, phase, nslot, slots...]
@@ -245,9 +271,8 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       SDMP_CHECK(n <= 32, "too many waits");
       uint32_t* ptrs[32];
       for (int64_t q = 0; q < n; ++q) ptrs[q] = p->local_flags + I[4 + q];
-      const uint32_t epoch = (uint32_t)(p->steps_done * p->phases + phase + 1);
-      return wait_flags(st, ptrs, (int)n, epoch,
-                        (unsigned long long)p->timeout_ms * 1000000ull, p->err_dev);
+      return wait_flags(st, ptrs, (int)n, 0, (unsigned long long)p->timeout_ms * 1000000ull,
+                        p->err_dev, p->dev_ctr, p->phases, (int)phase);
     }
     case SDMP_ACT_RECORD:
       SDMP_CHECK(I[2] >= 0 && I[2] < 32, "event id");
@@ -389,6 +414,13 @@ extern "C" int sdmp_plan_create(int32_t device, int32_t phases_per_step, sdmp_pl
   for (int k = 0; k < 32; ++k) SDMP_CUDA(cudaEventCreateWithFlags(&p->ev_user[k], cudaEventDisableTiming));
   SDMP_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
   SDMP_CUDA(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
+  SDMP_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  for (int c = 0; c < sdmp_plan::kCopy; ++c) {
+    SDMP_CUDA(cudaStreamCreateWithPriority(&p->cs[c], cudaStreamNonBlocking, hi));
+    SDMP_CUDA(cudaEventCreateWithFlags(&p->ev_cdone[c], cudaEventDisableTiming));
+  }
+  SDMP_CUDA(cudaMalloc((void**)&p->dev_ctr, 2 * sizeof(int64_t)));
+  SDMP_CUDA(cudaMemset(p->dev_ctr, 0, 2 * sizeof(int64_t)));
   SDMP_CUDA(cudaHostAlloc((void**)&p->err_host, sizeof(int), cudaHostAllocMapped));
   *p->err_host = 0;
   SDMP_CUDA(cudaHostGetDevicePointer((void**)&p->err_dev, p->err_host, 0));
@@ -410,10 +442,20 @@ extern "C" int sdmp_plan_destroy(sdmp_plan* p) {
   cudaEventDestroy(p->ev_step);
   cudaEventDestroy(p->ev_in);
   cudaEventDestroy(p->ev_out);
+  cudaEventDestroy(p->ev_fork);
+  for (int c = 0; c < sdmp_plan::kCopy; ++c) {
+    if (p->cs[c]) {
+      cudaStreamSynchronize(p->cs[c]);
+      cudaStreamDestroy(p->cs[c]);
+    }
+    cudaEventDestroy(p->ev_cdone[c]);
+  }
   for (auto e : p->tr_beg) cudaEventDestroy(e);
   for (auto e : p->tr_end) cudaEventDestroy(e);
   if (p->tr_origin) cudaEventDestroy(p->tr_origin);
   if (p->err_host) cudaFreeHost(p->err_host);
+  for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+  if (p->dev_ctr) cudaFree(p->dev_ctr);
   delete p;
   return SDMP_OK;
 }
@@ -555,10 +597,54 @@ static int trace_events(sdmp_plan* p, int64_t steps) {
 
 extern "C" int sdmp_plan_set_graph(sdmp_plan* p, int32_t on) {
   SDMP_CHECK(p, "null plan");
-  if (on) {
-    set_error("graph replay not enabled in this build");
-    return SDMP_EUNSUPPORTED;
+  p->graph_on = on != 0;
+  // replay period = lcm of the buffer counts (rotation repeats after it)
+  int per = 1;
+  for (const auto& f : p->fields) {
+    int a = per, b = f.nbuf;
+    while (b) { int t = a % b; a = b; b = t; }
+    per = per / a * f.nbuf;
   }
+  p->period = per;
+  return SDMP_OK;
+}
+
+// Enqueue one timestep.  `si` >= 0 records tracing events for step slot si.
+static int enqueue_step(sdmp_plan* p, int64_t time, int64_t si) {
+  const size_t nact = p->actions.size();
+  SDMP_CUDA(cudaEventRecord(p->ev_step, p->s[0]));
+  SDMP_CUDA(cudaStreamWaitEvent(p->s[1], p->ev_step, 0));
+  SDMP_CUDA(cudaStreamWaitEvent(p->s[2], p->ev_step, 0));
+  if (si >= 0) SDMP_CUDA(cudaEventRecord(p->tr_end[si], p->s[0]));
+  for (size_t k = 0; k < nact; ++k) {
+    cudaStream_t st = p->s[p->actions[k].i[1]];
+    if (si >= 0) SDMP_CUDA(cudaEventRecord(p->tr_beg[2 * (si * nact + k)], st));
+    int rc = run_action(p, p->actions[k], time);
+    if (rc) return rc;
+    if (si >= 0) SDMP_CUDA(cudaEventRecord(p->tr_beg[2 * (si * nact + k) + 1], st));
+  }
+  SDMP_CUDA(cudaEventRecord(p->ev_join[1], p->s[1]));
+  SDMP_CUDA(cudaEventRecord(p->ev_join[2], p->s[2]));
+  SDMP_CUDA(cudaStreamWaitEvent(p->s[0], p->ev_join[1], 0));
+  SDMP_CUDA(cudaStreamWaitEvent(p->s[0], p->ev_join[2], 0));
+  return tick_ctr(p->s[0], p->dev_ctr);
+}
+
+// Capture `period` steps starting at a time with residue r into a graph.
+static int capture_period(sdmp_plan* p, int64_t time, cudaGraphExec_t* out) {
+  cudaGraph_t g = nullptr;
+  SDMP_CUDA(cudaStreamBeginCapture(p->s[0], cudaStreamCaptureModeRelaxed));
+  int rc = SDMP_OK;
+  for (int k = 0; k < p->period && rc == SDMP_OK; ++k) rc = enqueue_step(p, time + k, -1);
+  cudaError_t e = cudaStreamEndCapture(p->s[0], &g);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  SDMP_CUDA(e);
+  cudaError_t ei = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  SDMP_CUDA(ei);
   return SDMP_OK;
 }
 
@@ -568,30 +654,37 @@ extern "C" int sdmp_plan_run(sdmp_plan* p, int64_t time_m, int64_t time_M, void*
   SDMP_CUDA(cudaSetDevice(p->device));
   cudaStream_t user = (cudaStream_t)stream;
   const int64_t nsteps = time_M - time_m + 1;
-  const size_t nact = p->actions.size();
   if (p->tracing && nsteps > 0) {
     int rc = trace_events(p, nsteps);
     if (rc) return rc;
   }
   SDMP_CUDA(cudaEventRecord(p->ev_in, user));
   SDMP_CUDA(cudaStreamWaitEvent(p->s[0], p->ev_in, 0));
-  for (int64_t time = time_m; time <= time_M; ++time) {
-    const int64_t si = time - time_m;
-    SDMP_CUDA(cudaEventRecord(p->ev_step, p->s[0]));
-    SDMP_CUDA(cudaStreamWaitEvent(p->s[1], p->ev_step, 0));
-    SDMP_CUDA(cudaStreamWaitEvent(p->s[2], p->ev_step, 0));
-    if (p->tracing) SDMP_CUDA(cudaEventRecord(p->tr_end[si], p->s[0]));
-    for (size_t k = 0; k < nact; ++k) {
-      cudaStream_t st = p->s[p->actions[k].i[1]];
-      if (p->tracing) SDMP_CUDA(cudaEventRecord(p->tr_beg[2 * (si * nact + k)], st));
-      int rc = run_action(p, p->actions[k], time);
-      if (rc) return rc;
-      if (p->tracing) SDMP_CUDA(cudaEventRecord(p->tr_beg[2 * (si * nact + k) + 1], st));
+  int rc = set_ctr(p->s[0], p->dev_ctr, time_m, p->steps_done);
+  if (rc) return rc;
+  int64_t time = time_m;
+  // graphs: only after the plan has run once (lazy attributes, scratch
+  // allocations and TMA descriptor entry points are resolved by then)
+  const bool graphs = p->graph_on && !p->tracing && p->period >= 1 && p->steps_done > 0;
+  while (time <= time_M) {
+    const int64_t left = time_M - time + 1;
+    if (graphs && left >= p->period) {
+      const int64_t r = ((time % p->period) + p->period) % p->period;
+      auto it = p->graphs.find(r);
+      if (it == p->graphs.end()) {
+        cudaGraphExec_t ex = nullptr;
+        rc = capture_period(p, time, &ex);
+        if (rc) return rc;
+        it = p->graphs.emplace(r, ex).first;
+      }
+      SDMP_CUDA(cudaGraphLaunch(it->second, p->s[0]));
+      time += p->period;
+      p->steps_done += p->period;
+      continue;
     }
-    SDMP_CUDA(cudaEventRecord(p->ev_join[1], p->s[1]));
-    SDMP_CUDA(cudaEventRecord(p->ev_join[2], p->s[2]));
-    SDMP_CUDA(cudaStreamWaitEvent(p->s[0], p->ev_join[1], 0));
-    SDMP_CUDA(cudaStreamWaitEvent(p->s[0], p->ev_join[2], 0));
+    rc = enqueue_step(p, time, p->tracing ? time - time_m : -1);
+    if (rc) return rc;
+    time += 1;
     p->steps_done += 1;
   }
   p->last_traced = p->tracing ? (int)nsteps : 0;

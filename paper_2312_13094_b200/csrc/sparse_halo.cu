@@ -10,12 +10,16 @@ namespace sdmp {
 
 // One thread per owned grid node; contributions pre-sorted by point id on
 // the host, summed sequentially: deterministic, no float atomics.
+// `ctr` (plan mode): device step counter {time, steps}; the series row is
+// ctr[0] - t0 (lets a captured CUDA graph replay across timesteps).
 __global__ void k_inject(float* __restrict__ f, const int64_t* __restrict__ node,
                          const int32_t* __restrict__ ptr, int nnodes,
                          const int32_t* __restrict__ pid, const float* __restrict__ w,
-                         const float* __restrict__ amps, float C, const float* __restrict__ m) {
+                         const float* __restrict__ amps, float C, const float* __restrict__ m,
+                         const int64_t* __restrict__ ctr, int64_t stride, int64_t t0) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= nnodes) return;
+  if (ctr) amps += (ctr[0] - t0) * stride;
   float acc = 0.f;
   for (int j = ptr[n]; j < ptr[n + 1]; ++j) acc = __fmaf_rn(w[j], amps[pid[j]], acc);
   const int64_t i = node[n];
@@ -24,28 +28,32 @@ __global__ void k_inject(float* __restrict__ f, const int64_t* __restrict__ node
 }
 
 __global__ void k_interp(const float* __restrict__ f, const int64_t* __restrict__ idx,
-                         const float* __restrict__ w, int npts, int nc, float* __restrict__ out) {
+                         const float* __restrict__ w, int npts, int nc, float* __restrict__ out,
+                         const int64_t* __restrict__ ctr, int64_t stride, int64_t t0) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= npts) return;
+  if (ctr) out += (ctr[0] - t0) * stride;
   float acc = 0.f;
   for (int c = 0; c < nc; ++c) acc = __fmaf_rn(w[p * nc + c], __ldg(f + idx[p * nc + c]), acc);
   out[p] = acc;
 }
 
 int inject(cudaStream_t st, float* field, const int64_t* node, const int32_t* ptr, int nnodes,
-           const int32_t* pid, const float* w, const float* amps, float C, const float* m) {
+           const int32_t* pid, const float* w, const float* amps, float C, const float* m,
+           const int64_t* ctr, int64_t stride, int64_t t0) {
   if (nnodes <= 0) return SDMP_OK;
   SDMP_CHECK(field && node && ptr && pid && w && amps, "inject: null array");
-  k_inject<<<(nnodes + 127) / 128, 128, 0, st>>>(field, node, ptr, nnodes, pid, w, amps, C, m);
+  k_inject<<<(nnodes + 127) / 128, 128, 0, st>>>(field, node, ptr, nnodes, pid, w, amps, C, m,
+                                                 ctr, stride, t0);
   SDMP_LAUNCHED();
   return SDMP_OK;
 }
 
 int interpolate(cudaStream_t st, const float* field, const int64_t* idx, const float* w,
-                int npts, int nc, float* out) {
+                int npts, int nc, float* out, const int64_t* ctr, int64_t stride, int64_t t0) {
   if (npts <= 0) return SDMP_OK;
   SDMP_CHECK(field && idx && w && out, "interpolate: null array");
-  k_interp<<<(npts + 127) / 128, 128, 0, st>>>(field, idx, w, npts, nc, out);
+  k_interp<<<(npts + 127) / 128, 128, 0, st>>>(field, idx, w, npts, nc, out, ctr, stride, t0);
   SDMP_LAUNCHED();
   return SDMP_OK;
 }
@@ -168,16 +176,23 @@ struct FlagArgs {
   int n;
   uint32_t value;
   unsigned long long timeout_ns;
-  int* err;  // host-mapped watchdog word
+  int* err;             // host-mapped watchdog word
+  const int64_t* ctr;   // plan mode: epoch = ctr[1] * phases + phase + 1
+  int phases, phase;
 };
+
+__device__ __forceinline__ uint32_t flag_value(const FlagArgs& a) {
+  return a.ctr ? (uint32_t)(a.ctr[1] * a.phases + a.phase + 1) : a.value;
+}
 
 // Writes `value` into each (peer) flag with system-scope release semantics,
 // after all prior work on the stream (copies into the peer's halo).
 __global__ void k_signal(FlagArgs a) {
   const int i = threadIdx.x;
   if (i >= a.n) return;
+  const uint32_t value = flag_value(a);
   __threadfence_system();
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.ptr[i]), "r"(a.value) : "memory");
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.ptr[i]), "r"(value) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -192,11 +207,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __global__ void k_wait(FlagArgs a) {
   const int i = threadIdx.x;
   if (i >= a.n) return;
+  const uint32_t value = flag_value(a);
   const unsigned long long t0 = gtimer();
   while (true) {
     uint32_t v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.ptr[i]) : "memory");
-    if ((int32_t)(v - a.value) >= 0) break;
+    if ((int32_t)(v - value) >= 0) break;
     if (gtimer() - t0 > a.timeout_ns) {
       atomicExch(a.err, 1);
       break;
@@ -205,20 +221,25 @@ __global__ void k_wait(FlagArgs a) {
   }
 }
 
-int signal_flags(cudaStream_t st, uint32_t* const* ptrs, int n, uint32_t value) {
+int signal_flags(cudaStream_t st, uint32_t* const* ptrs, int n, uint32_t value,
+                 const int64_t* ctr, int phases, int phase) {
   if (n <= 0) return SDMP_OK;
   SDMP_CHECK(n <= 32, "at most 32 flags per signal");
   FlagArgs a{};
   for (int i = 0; i < n; ++i) a.ptr[i] = ptrs[i];
   a.n = n;
   a.value = value;
+  a.ctr = ctr;
+  a.phases = phases;
+  a.phase = phase;
   k_signal<<<1, 32, 0, st>>>(a);
   SDMP_LAUNCHED();
   return SDMP_OK;
 }
 
 int wait_flags(cudaStream_t st, uint32_t* const* ptrs, int n, uint32_t value,
-               unsigned long long timeout_ns, int* err) {
+               unsigned long long timeout_ns, int* err, const int64_t* ctr, int phases,
+               int phase) {
   if (n <= 0) return SDMP_OK;
   SDMP_CHECK(n <= 32, "at most 32 flags per wait");
   FlagArgs a{};
@@ -227,7 +248,34 @@ int wait_flags(cudaStream_t st, uint32_t* const* ptrs, int n, uint32_t value,
   a.value = value;
   a.timeout_ns = timeout_ns;
   a.err = err;
+  a.ctr = ctr;
+  a.phases = phases;
+  a.phase = phase;
   k_wait<<<1, 32, 0, st>>>(a);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+// ---- plan step counter -------------------------------------------------------
+
+__global__ void k_set_ctr(int64_t* ctr, int64_t time, int64_t steps) {
+  ctr[0] = time;
+  ctr[1] = steps;
+}
+
+__global__ void k_tick(int64_t* ctr) {
+  ctr[0] += 1;
+  ctr[1] += 1;
+}
+
+int set_ctr(cudaStream_t st, int64_t* ctr, int64_t time, int64_t steps) {
+  k_set_ctr<<<1, 1, 0, st>>>(ctr, time, steps);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+int tick_ctr(cudaStream_t st, int64_t* ctr) {
+  k_tick<<<1, 1, 0, st>>>(ctr);
   SDMP_LAUNCHED();
   return SDMP_OK;
 }
@@ -239,12 +287,13 @@ using namespace sdmp;
 extern "C" int sdmp_inject(void* stream, float* field, const int64_t* node, const int32_t* ptr,
                            int32_t nnodes, const int32_t* pid, const float* w,
                            const float* amps, float C, const float* m) {
-  return inject((cudaStream_t)stream, field, node, ptr, nnodes, pid, w, amps, C, m);
+  return inject((cudaStream_t)stream, field, node, ptr, nnodes, pid, w, amps, C, m, nullptr, 0,
+                0);
 }
 
 extern "C" int sdmp_interpolate(void* stream, const float* field, const int64_t* idx,
                                 const float* w, int32_t npts, int32_t ncorner, float* out) {
-  return interpolate((cudaStream_t)stream, field, idx, w, npts, ncorner, out);
+  return interpolate((cudaStream_t)stream, field, idx, w, npts, ncorner, out, nullptr, 0, 0);
 }
 
 extern "C" int sdmp_bind_scale(void* stream, float* out, const float* in, int64_t n, float C) {

@@ -274,6 +274,11 @@ class NativePlan:
     def set_tracing(self, on: bool):
         check(lib().sdmp_plan_set_tracing(self.h, int(on)), "sdmp_plan_set_tracing", self.rank)
 
+    def set_graph(self, on: bool):
+        """Replay buffer-rotation periods as captured CUDA graphs (after the
+        first run of the plan)."""
+        check(lib().sdmp_plan_set_graph(self.h, int(on)), "sdmp_plan_set_graph", self.rank)
+
     def set_timeout(self, ms: int):
         check(lib().sdmp_plan_set_timeout(self.h, int(ms)), "sdmp_plan_set_timeout", self.rank)
 

@@ -164,6 +164,10 @@ class NativeOperatorPlan:
             self._encode(a, decomp, rank)
         if need_static:
             self._encode_static(ep, decomp, rank)
+        # CUDA-graph replay of whole buffer-rotation periods (SDMP_GRAPH=0
+        # disables); removes per-step launch overhead on small grids
+        import os
+        self.plan.set_graph(os.environ.get("SDMP_GRAPH", "1") != "0")
 
     # ------------------------------------------------------------------
     def _full_box(self, spec, box):

@@ -185,3 +185,27 @@ def test_stream_kernels_bitwise_equal_generic(family, so, monkeypatch):
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
         assert np.abs(a).max() > 0
+
+
+def test_graph_replay_long_run(monkeypatch):
+    res = []
+    for g in ("0", "1"):
+        monkeypatch.setenv("SDMP_GRAPH", g)
+        import paper_2312_13094_b200.api as A
+        A._FUNCS.clear()
+        shape = (24, 20, 28)
+        grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
+        kd = KD.acoustic_model(grid, so=8, name="ug")
+        u, m = kd.fields["u"], kd.fields["m"]
+        dt = float(np.float32(KD.critical_dt(4.6, grid.spacing)))
+        steps = 23
+        src = KD.point_source(grid, [tuple(0.5 * e + 1.3 for e in grid.extent)], steps, dt,
+                              f0=0.03, name="srcg")
+        rec = SparseTimeFunction("recg", grid, 5, steps,
+                                 coordinates=[(5.0 + 40 * i, 60.0, 70.0) for i in range(5)])
+        op = Operator([kd, src.inject(u.forward, expr=src * S.DT ** 2 / m), rec.interpolate(u)])
+        op.apply(time_M=2, dt=dt)          # first run: no graphs
+        op.apply(time_m=3, time_M=steps - 1, dt=dt)  # 20 steps: 6 periods + 2
+        res.append((u.data_gather(), rec.data.copy()))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert np.abs(res[1][1]).max() > 0
