@@ -263,9 +263,11 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
          const __grid_constant__ CUtensorMap tm_u2, const __grid_constant__ CUtensorMap tm_m,
          StarParams p, int xchunk) {
   using T = TmaCfg<R, TY>;
-  extern __shared__ unsigned char smraw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+  // __align__(1024) keeps TMA destinations aligned without integer pointer
+  // arithmetic, so the compiler still sees shared-space pointers (LDS, not
+  // generic LD) in the consumers
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = smraw;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(sm + T::S * T::STAGE);
   uint64_t* empty_bar = full_bar + T::S;
   const int lane = threadIdx.x, warp = threadIdx.y;

@@ -79,9 +79,11 @@ __global__ void __launch_bounds__(SLayout<R, TY, Op::NF, Op::NC, Op::NP>::THREAD
 stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, const int xchunk) {
   constexpr int NF = Op::NF, NC = Op::NC, NP = Op::NP;
   using L = SLayout<R, TY, NF, NC, NP>;
-  extern __shared__ unsigned char smraw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+  // __align__(1024) keeps TMA destinations aligned without integer pointer
+  // arithmetic, so the compiler still sees shared-space pointers (LDS, not
+  // generic LD) in the consumers
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = smraw;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(sm + L::S * L::STAGE);
   uint64_t* empty_bar = full_bar + L::S;
   const int lane = threadIdx.x, warp = threadIdx.y;
