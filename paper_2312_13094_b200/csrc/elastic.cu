@@ -29,101 +29,123 @@ struct ElCoef {
 // logical field ids
 enum { TXX = 0, TYY, TZZ, TXY, TXZ, TYZ, VX, VY, VZ, PB, NV_ = 10 };
 
+// First term as an explicit fma with a zero addend so that no separately
+// rounded product ever feeds an add (identical bits for float and V2).
 template <int R, int AX, int F, class A>
-__device__ __forceinline__ float dplus(const A& a, const float* c) {
-  float acc = __fmul_rn(c[0], __fsub_rn(a.template t<F, AX>(1), a.template t<F, AX>(0)));
+__device__ __forceinline__ typename A::T dplus(const A& a, const float* c) {
+  using T = typename A::T;
+  T acc = vcfma(c[0], vsub(a.template t<F, AX>(1), a.template t<F, AX>(0)), vconst<T>(0.f));
 #pragma unroll
   for (int k = 2; k <= R; ++k)
-    acc = __fmaf_rn(c[k - 1], __fsub_rn(a.template t<F, AX>(k), a.template t<F, AX>(1 - k)), acc);
+    acc = vcfma(c[k - 1], vsub(a.template t<F, AX>(k), a.template t<F, AX>(1 - k)), acc);
   return acc;
 }
 
 template <int R, int AX, int F, class A>
-__device__ __forceinline__ float dminus(const A& a, const float* c) {
-  float acc = __fmul_rn(c[0], __fsub_rn(a.template t<F, AX>(0), a.template t<F, AX>(-1)));
+__device__ __forceinline__ typename A::T dminus(const A& a, const float* c) {
+  using T = typename A::T;
+  T acc = vcfma(c[0], vsub(a.template t<F, AX>(0), a.template t<F, AX>(-1)), vconst<T>(0.f));
 #pragma unroll
   for (int k = 2; k <= R; ++k)
-    acc = __fmaf_rn(c[k - 1], __fsub_rn(a.template t<F, AX>(k - 1), a.template t<F, AX>(-k)), acc);
+    acc = vcfma(c[k - 1], vsub(a.template t<F, AX>(k - 1), a.template t<F, AX>(-k)), acc);
   return acc;
 }
 
 // ---- per-point routines (shared by both launch shapes) --------------------
 
 template <int R, class A>
-__device__ __forceinline__ void vel_point(const A& a, const ElCoef& k, float out[3]) {
-  const float bdt = __fmul_rn(k.dt, a.template p<PB>());
-  float dvx = __fadd_rn(__fadd_rn(dplus<R, 0, TXX>(a, k.c[0]), dminus<R, 1, TXY>(a, k.c[1])),
-                        dminus<R, 2, TXZ>(a, k.c[2]));
-  float dvy = __fadd_rn(__fadd_rn(dminus<R, 0, TXY>(a, k.c[0]), dplus<R, 1, TYY>(a, k.c[1])),
-                        dminus<R, 2, TYZ>(a, k.c[2]));
-  float dvz = __fadd_rn(__fadd_rn(dminus<R, 0, TXZ>(a, k.c[0]), dminus<R, 1, TYZ>(a, k.c[1])),
-                        dplus<R, 2, TZZ>(a, k.c[2]));
-  out[0] = __fmaf_rn(bdt, dvx, a.template p<VX>());
-  out[1] = __fmaf_rn(bdt, dvy, a.template p<VY>());
-  out[2] = __fmaf_rn(bdt, dvz, a.template p<VZ>());
+__device__ __forceinline__ void vel_point(const A& a, const ElCoef& k, typename A::T out[3]) {
+  using T = typename A::T;
+  const T bdt = vcmul(k.dt, a.template p<PB>());
+  T dvx = vadd(vadd(dplus<R, 0, TXX>(a, k.c[0]), dminus<R, 1, TXY>(a, k.c[1])),
+               dminus<R, 2, TXZ>(a, k.c[2]));
+  T dvy = vadd(vadd(dminus<R, 0, TXY>(a, k.c[0]), dplus<R, 1, TYY>(a, k.c[1])),
+               dminus<R, 2, TYZ>(a, k.c[2]));
+  T dvz = vadd(vadd(dminus<R, 0, TXZ>(a, k.c[0]), dminus<R, 1, TYZ>(a, k.c[1])),
+               dplus<R, 2, TZZ>(a, k.c[2]));
+  out[0] = vfma(bdt, dvx, a.template p<VX>());
+  out[1] = vfma(bdt, dvy, a.template p<VY>());
+  out[2] = vfma(bdt, dvz, a.template p<VZ>());
 }
 
 // strains from v (logical VX, VY, VZ): exx, eyy, ezz, exy, exz, eyz
 template <int R, class A>
-__device__ __forceinline__ void strain_point(const A& a, const ElCoef& k, float e[6]) {
+__device__ __forceinline__ void strain_point(const A& a, const ElCoef& k, typename A::T e[6]) {
   e[0] = dminus<R, 0, VX>(a, k.c[0]);
   e[1] = dminus<R, 1, VY>(a, k.c[1]);
   e[2] = dminus<R, 2, VZ>(a, k.c[2]);
-  e[3] = __fadd_rn(dplus<R, 1, VX>(a, k.c[1]), dplus<R, 0, VY>(a, k.c[0]));
-  e[4] = __fadd_rn(dplus<R, 2, VX>(a, k.c[2]), dplus<R, 0, VZ>(a, k.c[0]));
-  e[5] = __fadd_rn(dplus<R, 2, VY>(a, k.c[2]), dplus<R, 1, VZ>(a, k.c[1]));
+  e[3] = vadd(dplus<R, 1, VX>(a, k.c[1]), dplus<R, 0, VY>(a, k.c[0]));
+  e[4] = vadd(dplus<R, 2, VX>(a, k.c[2]), dplus<R, 0, VZ>(a, k.c[0]));
+  e[5] = vadd(dplus<R, 2, VY>(a, k.c[2]), dplus<R, 1, VZ>(a, k.c[1]));
 }
 
 // logical pointwise ids of the stress phases
 enum { S0 = 0, LAM = 6, MU = 7, R0 = 8, L2M = 14, MUS = 15, ITS = 16 };
 
 template <int R, class A>
-__device__ __forceinline__ void stress_point(const A& a, const ElCoef& k, float out[6]) {
-  float e[6];
+__device__ __forceinline__ void stress_point(const A& a, const ElCoef& k, typename A::T out[6]) {
+  using T = typename A::T;
+  T e[6];
   strain_point<R>(a, k, e);
-  const float l = a.template q<LAM>(), mu = a.template q<MU>();
-  const float tr = __fadd_rn(__fadd_rn(e[0], e[1]), e[2]);
-  const float ltr = __fmul_rn(l, tr), m2 = __fmul_rn(2.f, mu);
-  out[0] = __fmaf_rn(k.dt, __fmaf_rn(m2, e[0], ltr), a.template q<S0 + 0>());
-  out[1] = __fmaf_rn(k.dt, __fmaf_rn(m2, e[1], ltr), a.template q<S0 + 1>());
-  out[2] = __fmaf_rn(k.dt, __fmaf_rn(m2, e[2], ltr), a.template q<S0 + 2>());
-  out[3] = __fmaf_rn(k.dt, __fmul_rn(mu, e[3]), a.template q<S0 + 3>());
-  out[4] = __fmaf_rn(k.dt, __fmul_rn(mu, e[4]), a.template q<S0 + 4>());
-  out[5] = __fmaf_rn(k.dt, __fmul_rn(mu, e[5]), a.template q<S0 + 5>());
+  const T l = a.template q<LAM>(), mu = a.template q<MU>();
+  const T tr = vadd(vadd(e[0], e[1]), e[2]);
+  const T ltr = vmul(l, tr), m2 = vcmul(2.f, mu);
+  const T dt = vconst<T>(k.dt);
+  out[0] = vfma(dt, vfma(m2, e[0], ltr), a.template q<S0 + 0>());
+  out[1] = vfma(dt, vfma(m2, e[1], ltr), a.template q<S0 + 1>());
+  out[2] = vfma(dt, vfma(m2, e[2], ltr), a.template q<S0 + 2>());
+  out[3] = vfma(dt, vmul(mu, e[3]), a.template q<S0 + 3>());
+  out[4] = vfma(dt, vmul(mu, e[4]), a.template q<S0 + 4>());
+  out[5] = vfma(dt, vmul(mu, e[5]), a.template q<S0 + 5>());
 }
 
+// Memory-variable update: r1 = r0 - dt/ts (r0 + A),
+// s1 = s0 + dt (A + r1).  Shear A = M e is folded into explicit fmas
+// (r0 + M e, M e + r1) so no product is added separately.
 template <int C, class A>
-__device__ __forceinline__ void visco_comp(const A& a, const ElCoef& k, const float e[6],
-                                           float base, float m2, float M, float dti, float* s1,
-                                           float* r1) {
-  const float Ac = C < 3 ? __fmaf_rn(m2, e[C], base) : __fmul_rn(M, e[C]);
-  const float r0v = a.template q<R0 + C>();
-  const float rn = __fmaf_rn(-dti, __fadd_rn(r0v, Ac), r0v);
-  r1[C] = rn;
-  s1[C] = __fmaf_rn(k.dt, __fadd_rn(Ac, rn), a.template q<S0 + C>());
+__device__ __forceinline__ void visco_comp(const A& a, const ElCoef& k,
+                                           const typename A::T e[6], typename A::T base,
+                                           typename A::T m2, typename A::T M,
+                                           typename A::T ndti, typename A::T* s1,
+                                           typename A::T* r1) {
+  using T = typename A::T;
+  const T r0v = a.template q<R0 + C>();
+  const T dt = vconst<T>(k.dt);
+  if (C < 3) {
+    const T Ac = vfma(m2, e[C], base);
+    const T rn = vfma(ndti, vadd(r0v, Ac), r0v);
+    r1[C] = rn;
+    s1[C] = vfma(dt, vadd(Ac, rn), a.template q<S0 + C>());
+  } else {
+    const T rn = vfma(ndti, vfma(M, e[C], r0v), r0v);
+    r1[C] = rn;
+    s1[C] = vfma(dt, vfma(M, e[C], rn), a.template q<S0 + C>());
+  }
 }
 
 template <int R, class A>
-__device__ __forceinline__ void visco_point(const A& a, const ElCoef& k, float s1[6],
-                                            float r1[6]) {
-  float e[6];
+__device__ __forceinline__ void visco_point(const A& a, const ElCoef& k, typename A::T s1[6],
+                                            typename A::T r1[6]) {
+  using T = typename A::T;
+  T e[6];
   strain_point<R>(a, k, e);
-  const float L = a.template q<L2M>(), M = a.template q<MUS>(), I = a.template q<ITS>();
-  const float div = __fadd_rn(__fadd_rn(e[0], e[1]), e[2]);
-  const float base = __fmul_rn(__fsub_rn(L, __fmul_rn(2.f, M)), div);
-  const float m2 = __fmul_rn(2.f, M);
-  const float dti = __fmul_rn(k.dt, I);
-  visco_comp<0>(a, k, e, base, m2, M, dti, s1, r1);
-  visco_comp<1>(a, k, e, base, m2, M, dti, s1, r1);
-  visco_comp<2>(a, k, e, base, m2, M, dti, s1, r1);
-  visco_comp<3>(a, k, e, base, m2, M, dti, s1, r1);
-  visco_comp<4>(a, k, e, base, m2, M, dti, s1, r1);
-  visco_comp<5>(a, k, e, base, m2, M, dti, s1, r1);
+  const T L = a.template q<L2M>(), M = a.template q<MUS>(), I = a.template q<ITS>();
+  const T div = vadd(vadd(e[0], e[1]), e[2]);
+  const T m2 = vcmul(2.f, M);  // exact
+  const T base = vmul(vsub(L, m2), div);
+  const T ndti = vneg(vcmul(k.dt, I));
+  visco_comp<0>(a, k, e, base, m2, M, ndti, s1, r1);
+  visco_comp<1>(a, k, e, base, m2, M, ndti, s1, r1);
+  visco_comp<2>(a, k, e, base, m2, M, ndti, s1, r1);
+  visco_comp<3>(a, k, e, base, m2, M, ndti, s1, r1);
+  visco_comp<4>(a, k, e, base, m2, M, ndti, s1, r1);
+  visco_comp<5>(a, k, e, base, m2, M, ndti, s1, r1);
 }
 
 // ---- generic accessor: global memory ----------------------------------------
 
 struct GlobalAcc {
+  using T = float;
   const float* const* tap;  // indexed by logical tap field id
   const float* const* pnt;  // indexed by logical point id
   int64_t i, s[3];
@@ -186,17 +208,18 @@ __global__ void __launch_bounds__(256) visco_stress(ElGeneric p) {
 
 // velocity: fronts {txx, txy, txz}; centres {tyy, tzz, txy, txz, tyz};
 // points {vx, vy, vz, b}
-template <int R, int TY, int NF, int NC, int NP>
+template <class Ctx>
 struct VelAcc {
-  const StreamCtx<R, TY, NF, NC, NP>& c;
+  using T = typename Ctx::T;
+  const Ctx& c;
   template <int F, int AX>
-  __device__ __forceinline__ float t(int k) const {
+  __device__ __forceinline__ T t(int k) const {
     if (AX == 0) return c.xt(F == TXX ? 0 : F == TXY ? 1 : 2, k);
     constexpr int ci = F == TYY ? 0 : F == TZZ ? 1 : F == TXY ? 2 : F == TXZ ? 3 : 4;
     return AX == 1 ? c.ct(ci, k, 0) : c.ct(ci, 0, k);
   }
   template <int F>
-  __device__ __forceinline__ float p() const { return c.pt(F == VX ? 0 : F == VY ? 1 : F == VZ ? 2 : 3); }
+  __device__ __forceinline__ T p() const { return c.pt(F == VX ? 0 : F == VY ? 1 : F == VZ ? 2 : 3); }
 };
 
 struct VelOp {
@@ -204,31 +227,31 @@ struct VelOp {
   float* out[3];
   ElCoef k;
   template <int R, class Ctx>
-  __device__ __forceinline__ void point(const Ctx& c, int64_t idx) const {
-    VelAcc<R, Ctx::L::CY - 2 * R, NF, NC, NP> a{c};
-    float o[3];
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx, bool m0, bool m1) const {
+    VelAcc<Ctx> a{c};
+    typename Ctx::T o[3];
     vel_point<R>(a, k, o);
-    out[0][idx] = o[0];
-    out[1][idx] = o[1];
-    out[2][idx] = o[2];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) vstore(out[q], idx, o[q], m0, m1);
   }
 };
 
 // stress: fronts {vx, vy, vz}; centres {vx, vy, vz}; points: s0 (6) +
 // {lam, mu} or + r0 (6) + {l2m, mus, its}
-template <int R, int TY, int NF, int NC, int NP>
+template <class Ctx, int NPT>
 struct StrAcc {
-  const StreamCtx<R, TY, NF, NC, NP>& c;
+  using T = typename Ctx::T;
+  const Ctx& c;
   template <int F, int AX>
-  __device__ __forceinline__ float t(int k) const {
+  __device__ __forceinline__ T t(int k) const {
     constexpr int fi = F - VX;
     return AX == 0 ? c.xt(fi, k) : AX == 1 ? c.ct(fi, k, 0) : c.ct(fi, 0, k);
   }
   template <int Q>
-  __device__ __forceinline__ float q() const {
+  __device__ __forceinline__ T q() const {
     // elastic: S0..S0+5 -> 0..5, LAM -> 6, MU -> 7
     // visco:   S0..5 -> 0..5, R0..R0+5 -> 6..11, L2M/MUS/ITS -> 12..14
-    return c.pt(Q < 6 ? Q : (NP == 8 ? Q - LAM + 6 : (Q < L2M ? Q - R0 + 6 : Q - L2M + 12)));
+    return c.pt(Q < 6 ? Q : (NPT == 8 ? Q - LAM + 6 : (Q < L2M ? Q - R0 + 6 : Q - L2M + 12)));
   }
 };
 
@@ -237,12 +260,12 @@ struct StressOp {
   float* out[6];
   ElCoef k;
   template <int R, class Ctx>
-  __device__ __forceinline__ void point(const Ctx& c, int64_t idx) const {
-    StrAcc<R, Ctx::L::CY - 2 * R, NF, NC, NP> a{c};
-    float o[6];
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx, bool m0, bool m1) const {
+    StrAcc<Ctx, NP> a{c};
+    typename Ctx::T o[6];
     stress_point<R>(a, k, o);
 #pragma unroll
-    for (int q = 0; q < 6; ++q) out[q][idx] = o[q];
+    for (int q = 0; q < 6; ++q) vstore(out[q], idx, o[q], m0, m1);
   }
 };
 
@@ -251,17 +274,28 @@ struct ViscoOp {
   float* out[12];
   ElCoef k;
   template <int R, class Ctx>
-  __device__ __forceinline__ void point(const Ctx& c, int64_t idx) const {
-    StrAcc<R, Ctx::L::CY - 2 * R, NF, NC, NP> a{c};
-    float s1[6], r1[6];
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx, bool m0, bool m1) const {
+    StrAcc<Ctx, NP> a{c};
+    typename Ctx::T s1[6], r1[6];
     visco_point<R>(a, k, s1, r1);
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
-      out[q][idx] = s1[q];
-      out[6 + q][idx] = r1[q];
+      vstore(out[q], idx, s1[q], m0, m1);
+      vstore(out[6 + q], idx, r1[q], m0, m1);
     }
   }
 };
+
+// stream launch shape per radius: 2 z points per thread (packed fp32x2)
+// with 16 rows up to R = 4, 8 rows beyond (register budget)
+template <int R, class Op>
+static int launch_el_stream(const Op& op, const Geom& g, const int64_t full[3],
+                            const float* const* arrs, cudaStream_t st) {
+  constexpr bool big = Op::NP == 15;  // visco stress + memory variables
+  if constexpr (R <= 3) return launch_stream_op<R, 16, 2>(op, g, full, arrs, st);
+  else if constexpr (R == 4) return launch_stream_op<R, big ? 12 : 16, 2>(op, g, full, arrs, st);
+  else return launch_stream_op<R, 8, 2>(op, g, full, arrs, st);
+}
 
 // ---- host ----------------------------------------------------------------
 
@@ -339,8 +373,7 @@ extern "C" int sdmp_elastic_velocity(void* stream, const float* const v0[3],
     VelOp op{};
     for (int c = 0; c < 3; ++c) op.out[c] = v1[c];
     op.k = p.k;
-    RADIUS_SWITCH((RR <= 4 ? launch_stream_op<RR, 16>(op, p.g, full, arrs, st)
-                           : launch_stream_op<RR, 8>(op, p.g, full, arrs, st)))
+    RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st))
   }
   RADIUS_SWITCH(launch_generic(p.g, el_velocity<RR>, p, st))
 }
@@ -367,8 +400,7 @@ extern "C" int sdmp_elastic_stress(void* stream, const float* const v1[3],
     StressOp op{};
     for (int c = 0; c < 6; ++c) op.out[c] = t1[c];
     op.k = p.k;
-    RADIUS_SWITCH((RR <= 4 ? launch_stream_op<RR, 16>(op, p.g, full, arrs, st)
-                           : launch_stream_op<RR, 8>(op, p.g, full, arrs, st)))
+    RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st))
   }
   RADIUS_SWITCH(launch_generic(p.g, el_stress<RR>, p, st))
 }
@@ -402,8 +434,7 @@ extern "C" int sdmp_visco_stress(void* stream, const float* const v1[3],
     ViscoOp op{};
     for (int c = 0; c < 12; ++c) op.out[c] = p.out[c];
     op.k = p.k;
-    RADIUS_SWITCH((RR <= 4 ? launch_stream_op<RR, 16>(op, p.g, full, arrs, st)
-                           : launch_stream_op<RR, 8>(op, p.g, full, arrs, st)))
+    RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st))
   }
   RADIUS_SWITCH(launch_generic(p.g, visco_stress<RR>, p, st))
 }

@@ -1,13 +1,14 @@
 // Generic TMA streaming engine for multi-field stencils on sm_100a.
 //
-// A CTA owns a 32(z) x TY(y) tile and streams along x.  One producer warp
-// fills an S-stage shared-memory ring with cp.async.bulk.tensor 3D tile
-// loads (mbarrier complete_tx); TY consumer warps compute one point per
-// thread (z = lane, y = warp).  Per pipeline iteration i (plane xa-R+i):
+// A CTA owns a (32*V)(z) x TY(y) tile and streams along x.  One producer
+// warp fills an S-stage shared-memory ring with cp.async.bulk.tensor 3D tile
+// loads (mbarrier complete_tx); TY consumer warps compute V consecutive z
+// points per thread (V = 2: packed fp32x2 arithmetic, 64-bit LDS/STG).
+// Per pipeline iteration i (plane xa-R+i):
 //
-//   NF "front" tiles  [TY][32]              -> per-field x-window registers
-//   NC "centre" tiles [TY+2R][32+2*OFF]     -> y / z taps (TMA zero-fills OOB)
-//   NP "point" tiles  [TY][32]              -> pointwise operands
+//   NF "front" tiles  [TY][32V]              -> per-field x-window registers
+//   NC "centre" tiles [TY+2R][32V+2*OFF]     -> y / z taps (TMA zero-fills OOB)
+//   NP "point" tiles  [TY][32V]              -> pointwise operands
 //
 // front tiles run 2R planes ahead of the centre/point tiles, so at
 // iteration i >= 2R the consumer holds planes x-R..x+R of every front field
@@ -15,33 +16,37 @@
 //
 // The operator `Op` supplies
 //   static constexpr int NF, NC, NP;
-//   __device__ void point(const StreamCtx<...>&, int64_t idx) const;
+//   template <int R, class Ctx> __device__ void point(const Ctx&, int64_t idx,
+//                                                      bool m0, bool m1) const;
 // and the per-point arithmetic is shared with the one-thread-per-point
-// generic kernels through accessor templates (bit-identical results).
+// generic kernels through accessor / value-type templates (vmath.cuh), so
+// both launch shapes give identical bits.
 #pragma once
 
 #include <cstdio>
 #include <cstdlib>
 
 #include "tma.cuh"
+#include "vmath.cuh"
 
 namespace sdmp {
 
-constexpr int kSZ = 32;  // z points per tile (one per lane)
+constexpr int kSZ = 32;  // lanes along z
 
 __host__ __device__ constexpr int sround4(int r) { return (r + 3) & ~3; }
 
-template <int R, int TY, int NF, int NC, int NP>
+template <int R, int TY, int V, int NF, int NC, int NP>
 struct SLayout {
+  static constexpr int TZ = kSZ * V;
   static constexpr int OFF = sround4(R);
-  static constexpr int CZ = kSZ + 2 * OFF;
+  static constexpr int CZ = TZ + 2 * OFF;
   static constexpr int CY = TY + 2 * R;
-  static constexpr int FRONT = kSZ * TY * 4;
+  static constexpr int FRONT = TZ * TY * 4;
   static constexpr int CENTER = ((CZ * CY * 4) + 127) & ~127;
   static constexpr int STAGE = NF * FRONT + NC * CENTER + NP * FRONT;
   static constexpr int S0 = (200 * 1024) / STAGE;
   static constexpr int S = S0 > 4 ? 4 : (S0 < 2 ? 2 : S0);
-  static constexpr int BYTES = S * STAGE + 2 * S * 8 + 128;
+  static constexpr int BYTES = S * STAGE + 2 * S * 8;
   static constexpr int THREADS = 32 * (TY + 1);
   static constexpr uint32_t TX_FRONT = NF * FRONT;
   static constexpr uint32_t TX_MAIN = NF * FRONT + NC * CZ * CY * 4 + NP * FRONT;
@@ -52,36 +57,73 @@ struct TMaps {
   CUtensorMap m[kMaxMaps];
 };
 
-// Consumer-side view of one point.
-template <int R, int TY, int NF, int NC, int NP>
+template <int V> struct VType;
+template <> struct VType<1> { using T = float; };
+template <> struct VType<2> { using T = V2; };
+
+template <int V>
+__device__ __forceinline__ typename VType<V>::T vload(const float* p);
+template <>
+__device__ __forceinline__ float vload<1>(const float* p) { return *p; }
+template <>
+__device__ __forceinline__ V2 vload<2>(const float* p) {
+  V2 o;
+  o.r = *reinterpret_cast<const uint64_t*>(p);
+  return o;
+}
+
+// Consumer-side view of one thread's V points.
+template <int R, int TY, int V, int NF, int NC, int NP>
 struct StreamCtx {
-  using L = SLayout<R, TY, NF, NC, NP>;
-  const float (*w)[2 * R + 1];   // x-windows
+  using L = SLayout<R, TY, V, NF, NC, NP>;
+  using T = typename VType<V>::T;
+  const T (*w)[2 * R + 1];   // x-windows
   const unsigned char* stage;
   int warp, lane;
-  // field f (front index) at x + k
-  __device__ __forceinline__ float xt(int f, int k) const { return w[f][R + k]; }
-  // centre tile c at (y + dy, z + dz)
-  __device__ __forceinline__ float ct(int c, int dy, int dz) const {
+  __device__ __forceinline__ T xt(int f, int k) const { return w[f][R + k]; }
+  __device__ __forceinline__ const float* crow(int c, int dy) const {
     const float* base = reinterpret_cast<const float*>(stage + NF * L::FRONT + c * L::CENTER);
-    return base[(warp + R + dy) * L::CZ + L::OFF + lane + dz];
+    return base + (warp + R + dy) * L::CZ + L::OFF + V * lane;
   }
-  // point tile q
-  __device__ __forceinline__ float pt(int q) const {
+  // centre tile c at (y + dy, z + dz)
+  __device__ __forceinline__ T ct(int c, int dy, int dz) const {
+    const float* p = crow(c, dy) + dz;
+    if constexpr (V == 2) {
+      if (dz & 1) {  // odd shift of a packed pair: from the two aligned pairs
+        const V2 lo = vload<2>(p - 1), hi = vload<2>(p + 1);
+        return v2pack(v2hi(lo), v2lo(hi));
+      }
+    }
+    return vload<V>(p);
+  }
+  __device__ __forceinline__ T pt(int q) const {
     const float* base = reinterpret_cast<const float*>(stage + NF * L::FRONT + NC * L::CENTER +
                                                        q * L::FRONT);
-    return base[warp * kSZ + lane];
+    return vload<V>(base + warp * L::TZ + V * lane);
   }
 };
 
-template <int R, int TY, class Op>
-__global__ void __launch_bounds__(SLayout<R, TY, Op::NF, Op::NC, Op::NP>::THREADS, 1)
+// masked store of V consecutive values at idx (m0: first point, m1: second)
+__device__ __forceinline__ void vstore(float* p, int64_t idx, float v, bool m0, bool) {
+  if (m0) p[idx] = v;
+}
+__device__ __forceinline__ void vstore(float* p, int64_t idx, V2 v, bool m0, bool m1) {
+  if (m0 && m1) {
+    *reinterpret_cast<uint64_t*>(p + idx) = v.r;
+  } else {
+    if (m0) p[idx] = v2lo(v);
+    if (m1) p[idx + 1] = v2hi(v);
+  }
+}
+
+template <int R, int TY, int V, class Op>
+__global__ void __launch_bounds__(SLayout<R, TY, V, Op::NF, Op::NC, Op::NP>::THREADS, 1)
 stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, const int xchunk) {
   constexpr int NF = Op::NF, NC = Op::NC, NP = Op::NP;
-  using L = SLayout<R, TY, NF, NC, NP>;
+  using L = SLayout<R, TY, V, NF, NC, NP>;
+  using T = typename VType<V>::T;
   // __align__(1024) keeps TMA destinations aligned without integer pointer
-  // arithmetic, so the compiler still sees shared-space pointers (LDS, not
-  // generic LD) in the consumers
+  // arithmetic, so the consumers keep shared-space pointers (LDS)
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = smraw;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(sm + L::S * L::STAGE);
@@ -96,8 +138,8 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
   }
   __syncthreads();
   // TMA boxes must start on a 16 B boundary along z: tiles are aligned down
-  // to a multiple of 4 floats and lanes left of the box are masked off.
-  const int z0 = (g.lo[2] & ~3) + blockIdx.x * kSZ;
+  // to a multiple of 4 floats and lanes outside the box are masked off.
+  const int z0 = (g.lo[2] & ~3) + blockIdx.x * L::TZ;
   const int y0 = g.lo[1] + blockIdx.y * TY;
   const int xa = g.lo[0] + blockIdx.z * xchunk;
   const int xb = min(xa + xchunk, g.hi[0]);
@@ -131,13 +173,16 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
     return;
   }
 
-  const int z = z0 + lane, y = y0 + warp;
-  const bool active = (z >= g.lo[2]) && (z < g.hi[2]) && (y < g.hi[1]);
-  float w[NF > 0 ? NF : 1][2 * R + 1];
+  const int z = z0 + V * lane, y = y0 + warp;
+  const bool yin = y < g.hi[1];
+  const bool m0 = yin && z >= g.lo[2] && z < g.hi[2];
+  const bool m1 = V > 1 && yin && z + 1 >= g.lo[2] && z + 1 < g.hi[2];
+  const bool active = m0 || m1;
+  T w[NF > 0 ? NF : 1][2 * R + 1];
 #pragma unroll
   for (int f = 0; f < NF; ++f)
 #pragma unroll
-    for (int k = 0; k <= 2 * R; ++k) w[f][k] = 0.f;
+    for (int k = 0; k <= 2 * R; ++k) w[f][k] = vconst<T>(0.f);
 
   for (int i = 0; i < nit; ++i) {
     const int s = i % L::S;
@@ -147,12 +192,13 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
     for (int f = 0; f < NF; ++f) {
 #pragma unroll
       for (int k = 0; k < 2 * R; ++k) w[f][k] = w[f][k + 1];
-      w[f][2 * R] = reinterpret_cast<const float*>(st + f * L::FRONT)[warp * kSZ + lane];
+      w[f][2 * R] = vload<V>(reinterpret_cast<const float*>(st + f * L::FRONT) +
+                             warp * L::TZ + V * lane);
     }
     if (i >= 2 * R && active) {
       const int x = xa + i - 2 * R;
-      StreamCtx<R, TY, NF, NC, NP> ctx{w, st, warp, lane};
-      op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z);
+      StreamCtx<R, TY, V, NF, NC, NP> ctx{w, st, warp, lane};
+      op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0, m1);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
@@ -179,23 +225,23 @@ inline int stream_chunks(int64_t tiles, int nx, int R) {
 
 // Host launcher: `ptrs` = NF front arrays, then NC centre arrays, then NP
 // point arrays (all FULL-shaped, same `full`).
-template <int R, int TY, class Op>
+template <int R, int TY, int V, class Op>
 int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const float* const* ptrs,
                      cudaStream_t st) {
-  using L = SLayout<R, TY, Op::NF, Op::NC, Op::NP>;
+  using L = SLayout<R, TY, V, Op::NF, Op::NC, Op::NP>;
   static_assert(Op::NF + Op::NC + Op::NP <= kMaxMaps, "too many tensor maps");
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    SDMP_CUDA(cudaFuncSetAttribute(stream_kernel<R, TY, Op>,
+    SDMP_CUDA(cudaFuncSetAttribute(stream_kernel<R, TY, V, Op>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
     attr_dev = dev;
   }
   TMaps maps;
   int k = 0;
   for (int f = 0; f < Op::NF; ++f, ++k) {
-    int rc = make_tmap_3d(&maps.m[k], ptrs[k], full, kSZ, TY, false);
+    int rc = make_tmap_3d(&maps.m[k], ptrs[k], full, L::TZ, TY, false);
     if (rc) return rc;
   }
   for (int c = 0; c < Op::NC; ++c, ++k) {
@@ -203,11 +249,11 @@ int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const f
     if (rc) return rc;
   }
   for (int q = 0; q < Op::NP; ++q, ++k) {
-    int rc = make_tmap_3d(&maps.m[k], ptrs[k], full, kSZ, TY, true);
+    int rc = make_tmap_3d(&maps.m[k], ptrs[k], full, L::TZ, TY, true);
     if (rc) return rc;
   }
   const int nz = g.hi[2] - g.lo[2], ny = g.hi[1] - g.lo[1], nx = g.hi[0] - g.lo[0];
-  const int tz = (nz + (g.lo[2] & 3) + kSZ - 1) / kSZ, ty = (ny + TY - 1) / TY;
+  const int tz = (nz + (g.lo[2] & 3) + L::TZ - 1) / L::TZ, ty = (ny + TY - 1) / TY;
   int nch = stream_chunks((int64_t)tz * ty, nx, R);
   const int chunk = (nx + nch - 1) / nch;
   nch = (nx + chunk - 1) / chunk;
@@ -216,12 +262,12 @@ int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const f
   const bool dbg = getenv("SDMP_DEBUG") != nullptr;
   if (dbg)
     fprintf(stderr,
-            "[sdmp] stream_kernel R=%d TY=%d NF=%d NC=%d NP=%d box=[%d,%d,%d]-[%d,%d,%d] "
+            "[sdmp] stream_kernel R=%d TY=%d V=%d NF=%d NC=%d NP=%d box=[%d,%d,%d]-[%d,%d,%d] "
             "full=[%ld,%ld,%ld] grid=(%d,%d,%d) chunk=%d smem=%d S=%d stage=%d\n",
-            R, TY, Op::NF, Op::NC, Op::NP, g.lo[0], g.lo[1], g.lo[2], g.hi[0], g.hi[1], g.hi[2],
-            (long)full[0], (long)full[1], (long)full[2], tz, ty, nch, chunk, L::BYTES, L::S,
-            L::STAGE);
-  stream_kernel<R, TY, Op><<<grid, block, L::BYTES, st>>>(maps, op, g, chunk);
+            R, TY, V, Op::NF, Op::NC, Op::NP, g.lo[0], g.lo[1], g.lo[2], g.hi[0], g.hi[1],
+            g.hi[2], (long)full[0], (long)full[1], (long)full[2], tz, ty, nch, chunk, L::BYTES,
+            L::S, L::STAGE);
+  stream_kernel<R, TY, V, Op><<<grid, block, L::BYTES, st>>>(maps, op, g, chunk);
   SDMP_LAUNCHED();
   if (dbg) {
     cudaError_t e = cudaStreamSynchronize(st);

@@ -37,73 +37,85 @@ struct TTICoef {
 enum { TP = 0, TR, TAX, TAY, TAZ, TGP, TGR, NT_ };
 enum { QP2 = 0, QR0, QR2, QM, QE, QD, QAX, QAY, QAZ, NQ_ };
 
+// All sums start from an explicit fma with a zero addend and products are
+// folded into fmas, so no separately rounded product feeds an add (ptxas
+// contracts packed mul+add): float and V2 evaluations give identical bits.
 template <int R, int AX, int F, class A>
-__device__ __forceinline__ float dcentral(const A& a, const float* w) {
-  float acc = __fmul_rn(w[1], __fsub_rn(a.template t<F, AX>(1), a.template t<F, AX>(-1)));
+__device__ __forceinline__ typename A::T dcentral(const A& a, const float* w) {
+  using T = typename A::T;
+  T acc = vcfma(w[1], vsub(a.template t<F, AX>(1), a.template t<F, AX>(-1)), vconst<T>(0.f));
 #pragma unroll
   for (int k = 2; k <= R; ++k)
-    acc = __fmaf_rn(w[k], __fsub_rn(a.template t<F, AX>(k), a.template t<F, AX>(-k)), acc);
+    acc = vcfma(w[k], vsub(a.template t<F, AX>(k), a.template t<F, AX>(-k)), acc);
   return acc;
 }
 
-// D_AX (a_AX g) with a, g both tapped
+// D_AX (a_AX g) with a, g both tapped: term_k = a(k) g(k) - a(-k) g(-k)
+// evaluated as fma(a(k), g(k), -(a(-k) g(-k))).
 template <int R, int AX, int FA, int FG, class A>
-__device__ __forceinline__ float outer(const A& a, const float* w) {
-  float acc = 0.f;
+__device__ __forceinline__ typename A::T outer(const A& a, const float* w) {
+  using T = typename A::T;
+  T acc = vconst<T>(0.f);
 #pragma unroll
   for (int k = 1; k <= R; ++k) {
-    const float hi = __fmul_rn(a.template t<FA, AX>(k), a.template t<FG, AX>(k));
-    const float lo = __fmul_rn(a.template t<FA, AX>(-k), a.template t<FG, AX>(-k));
-    acc = k == 1 ? __fmul_rn(w[1], __fsub_rn(hi, lo)) : __fmaf_rn(w[k], __fsub_rn(hi, lo), acc);
+    const T lo = vmul(a.template t<FA, AX>(-k), a.template t<FG, AX>(-k));
+    const T term = vfma(a.template t<FA, AX>(k), a.template t<FG, AX>(k), vneg(lo));
+    acc = vcfma(w[k], term, acc);
   }
   return acc;
 }
 
 template <int R, class A>
-__device__ __forceinline__ void g_point(const A& a, const TTICoef& c, float& gp, float& gr) {
-  const float ax = a.template q<QAX>(), ay = a.template q<QAY>(), az = a.template q<QAZ>();
-  gp = __fmul_rn(ax, dcentral<R, 0, TP>(a, c.d1[0]));
-  gp = __fmaf_rn(ay, dcentral<R, 1, TP>(a, c.d1[1]), gp);
-  gp = __fmaf_rn(az, dcentral<R, 2, TP>(a, c.d1[2]), gp);
-  gr = __fmul_rn(ax, dcentral<R, 0, TR>(a, c.d1[0]));
-  gr = __fmaf_rn(ay, dcentral<R, 1, TR>(a, c.d1[1]), gr);
-  gr = __fmaf_rn(az, dcentral<R, 2, TR>(a, c.d1[2]), gr);
+__device__ __forceinline__ void g_point(const A& a, const TTICoef& c, typename A::T& gp,
+                                        typename A::T& gr) {
+  using T = typename A::T;
+  const T ax = a.template q<QAX>(), ay = a.template q<QAY>(), az = a.template q<QAZ>();
+  gp = vfma(ax, dcentral<R, 0, TP>(a, c.d1[0]), vconst<T>(0.f));
+  gp = vfma(ay, dcentral<R, 1, TP>(a, c.d1[1]), gp);
+  gp = vfma(az, dcentral<R, 2, TP>(a, c.d1[2]), gp);
+  gr = vfma(ax, dcentral<R, 0, TR>(a, c.d1[0]), vconst<T>(0.f));
+  gr = vfma(ay, dcentral<R, 1, TR>(a, c.d1[1]), gr);
+  gr = vfma(az, dcentral<R, 2, TR>(a, c.d1[2]), gr);
 }
 
 template <int R, class A>
-__device__ __forceinline__ void u_point(const A& a, const TTICoef& c, float& p1, float& r1) {
-  float gzp = outer<R, 0, TAX, TGP>(a, c.d1[0]);
-  gzp = __fadd_rn(gzp, outer<R, 1, TAY, TGP>(a, c.d1[1]));
-  gzp = __fadd_rn(gzp, outer<R, 2, TAZ, TGP>(a, c.d1[2]));
-  float gzr = outer<R, 0, TAX, TGR>(a, c.d1[0]);
-  gzr = __fadd_rn(gzr, outer<R, 1, TAY, TGR>(a, c.d1[1]));
-  gzr = __fadd_rn(gzr, outer<R, 2, TAZ, TGR>(a, c.d1[2]));
-  const float c0 = a.template t<TP, 0>(0);
-  float lap = __fmul_rn(c.csum0, c0);
+__device__ __forceinline__ void u_point(const A& a, const TTICoef& c, typename A::T& p1,
+                                        typename A::T& r1) {
+  using T = typename A::T;
+  T gzp = outer<R, 0, TAX, TGP>(a, c.d1[0]);
+  gzp = vadd(gzp, outer<R, 1, TAY, TGP>(a, c.d1[1]));
+  gzp = vadd(gzp, outer<R, 2, TAZ, TGP>(a, c.d1[2]));
+  T gzr = outer<R, 0, TAX, TGR>(a, c.d1[0]);
+  gzr = vadd(gzr, outer<R, 1, TAY, TGR>(a, c.d1[1]));
+  gzr = vadd(gzr, outer<R, 2, TAZ, TGR>(a, c.d1[2]));
+  const T c0 = a.template t<TP, 0>(0);
+  T lap = vcfma(c.csum0, c0, vconst<T>(0.f));
 #pragma unroll
   for (int k = 1; k <= R; ++k)
-    lap = __fmaf_rn(c.lap[0][k], __fadd_rn(a.template t<TP, 0>(-k), a.template t<TP, 0>(k)), lap);
+    lap = vcfma(c.lap[0][k], vadd(a.template t<TP, 0>(-k), a.template t<TP, 0>(k)), lap);
 #pragma unroll
   for (int k = 1; k <= R; ++k)
-    lap = __fmaf_rn(c.lap[1][k], __fadd_rn(a.template t<TP, 1>(-k), a.template t<TP, 1>(k)), lap);
+    lap = vcfma(c.lap[1][k], vadd(a.template t<TP, 1>(-k), a.template t<TP, 1>(k)), lap);
 #pragma unroll
   for (int k = 1; k <= R; ++k)
-    lap = __fmaf_rn(c.lap[2][k], __fadd_rn(a.template t<TP, 2>(-k), a.template t<TP, 2>(k)), lap);
-  const float h0 = __fsub_rn(lap, gzp);
-  const float sc = __fdiv_rn(c.dt2, a.template q<QM>());
-  const float e = a.template q<QE>(), d = a.template q<QD>();
-  const float pp = __fmaf_rn(d, gzr, __fmul_rn(e, h0));
-  const float rr = __fmaf_rn(d, h0, gzr);
-  const float pt = __fsub_rn(__fmul_rn(2.f, c0), a.template q<QP2>());
-  const float r0v = a.template q<QR0>();
-  const float rt = __fsub_rn(__fmul_rn(2.f, r0v), a.template q<QR2>());
-  p1 = __fmaf_rn(sc, pp, pt);
-  r1 = __fmaf_rn(sc, rr, rt);
+    lap = vcfma(c.lap[2][k], vadd(a.template t<TP, 2>(-k), a.template t<TP, 2>(k)), lap);
+  const T h0 = vsub(lap, gzp);
+  const T sc = vdiv(vconst<T>(c.dt2), a.template q<QM>());
+  const T e = a.template q<QE>(), d = a.template q<QD>();
+  const T pp = vfma(d, gzr, vmul(e, h0));
+  const T rr = vfma(d, h0, gzr);
+  const T two = vconst<T>(2.f);
+  const T pt = vfma(two, c0, vneg(a.template q<QP2>()));   // 2 c0 exact
+  const T r0v = a.template q<QR0>();
+  const T rt = vfma(two, r0v, vneg(a.template q<QR2>()));
+  p1 = vfma(sc, pp, pt);
+  r1 = vfma(sc, rr, rt);
 }
 
 // ---- generic launch ---------------------------------------------------------
 
 struct TTIGlobalAcc {
+  using T = float;
   const float* const* tap;
   const float* const* pnt;
   int64_t i, s[3];
@@ -152,16 +164,17 @@ __global__ void __launch_bounds__(256) tti_update(TTIGeneric p) {
 // ---- stream operators --------------------------------------------------------
 
 // pass 1: fronts {p, r}; centres {p, r}; points {ax, ay, az}
-template <int R, int TY, int NF, int NC, int NP>
+template <class Ctx>
 struct GAcc {
-  const StreamCtx<R, TY, NF, NC, NP>& c;
+  using T = typename Ctx::T;
+  const Ctx& c;
   template <int F, int AX>
-  __device__ __forceinline__ float t(int k) const {
+  __device__ __forceinline__ T t(int k) const {
     constexpr int fi = F == TP ? 0 : 1;
     return AX == 0 ? c.xt(fi, k) : AX == 1 ? c.ct(fi, k, 0) : c.ct(fi, 0, k);
   }
   template <int Q>
-  __device__ __forceinline__ float q() const { return c.pt(Q - QAX); }
+  __device__ __forceinline__ T q() const { return c.pt(Q - QAX); }
 };
 
 struct GOp {
@@ -169,28 +182,29 @@ struct GOp {
   float* out[2];
   TTICoef k;
   template <int R, class Ctx>
-  __device__ __forceinline__ void point(const Ctx& c, int64_t idx) const {
-    GAcc<R, Ctx::L::CY - 2 * R, NF, NC, NP> a{c};
-    float gp, gr;
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx, bool m0, bool m1) const {
+    GAcc<Ctx> a{c};
+    typename Ctx::T gp, gr;
     g_point<R>(a, k, gp, gr);
-    out[0][idx] = gp;
-    out[1][idx] = gr;
+    vstore(out[0], idx, gp, m0, m1);
+    vstore(out[1], idx, gr, m0, m1);
   }
 };
 
 // pass 2: fronts {ax, gp, gr, p}; centres {ay, az, gp, gr, p};
 // points {p2, r0, r2, m, epsp, delp}
-template <int R, int TY, int NF, int NC, int NP>
+template <class Ctx>
 struct UAcc {
-  const StreamCtx<R, TY, NF, NC, NP>& c;
+  using T = typename Ctx::T;
+  const Ctx& c;
   template <int F, int AX>
-  __device__ __forceinline__ float t(int k) const {
+  __device__ __forceinline__ T t(int k) const {
     if (AX == 0) return c.xt(F == TAX ? 0 : F == TGP ? 1 : F == TGR ? 2 : 3, k);
     constexpr int ci = F == TAY ? 0 : F == TAZ ? 1 : F == TGP ? 2 : F == TGR ? 3 : 4;
     return AX == 1 ? c.ct(ci, k, 0) : c.ct(ci, 0, k);
   }
   template <int Q>
-  __device__ __forceinline__ float q() const { return c.pt(Q); }
+  __device__ __forceinline__ T q() const { return c.pt(Q); }
 };
 
 struct UOp {
@@ -198,14 +212,27 @@ struct UOp {
   float* out[2];
   TTICoef k;
   template <int R, class Ctx>
-  __device__ __forceinline__ void point(const Ctx& c, int64_t idx) const {
-    UAcc<R, Ctx::L::CY - 2 * R, NF, NC, NP> a{c};
-    float p1, r1;
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx, bool m0, bool m1) const {
+    UAcc<Ctx> a{c};
+    typename Ctx::T p1, r1;
     u_point<R>(a, k, p1, r1);
-    out[0][idx] = p1;
-    out[1][idx] = r1;
+    vstore(out[0], idx, p1, m0, m1);
+    vstore(out[1], idx, r1, m0, m1);
   }
 };
+
+// Launch shape per radius (rows TY, z points per thread V): packed fp32x2
+// (V = 2) while the per-thread registers fit without spills (ptxas -v),
+// fewer rows as R grows; scalar for the widest update stencils.
+template <int R, class Op>
+static int launch_tti_stream(const Op& op, const Geom& g, const int64_t full[3],
+                             const float* const* arrs, cudaStream_t st) {
+  constexpr bool upd = Op::NF == 4;
+  if constexpr (R <= 3) return launch_stream_op<R, 16, 2>(op, g, full, arrs, st);
+  else if constexpr (R == 4) return launch_stream_op<R, upd ? 12 : 16, 2>(op, g, full, arrs, st);
+  else if constexpr (!upd || R == 5) return launch_stream_op<R, 8, 2>(op, g, full, arrs, st);
+  else return launch_stream_op<R, 8, 1>(op, g, full, arrs, st);
+}
 
 // FULL-shaped scratch pair per (device, size), grow-only, never freed
 // before process exit (the plan reuses it every step).
@@ -260,15 +287,13 @@ static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3]) {
     g.out[0] = p1.out[0];
     g.out[1] = p1.out[1];
     g.k = p.c;
-    int rc = R <= 4 ? launch_stream_op<R, 16>(g, p1.g, full, a1, st)
-                    : launch_stream_op<R, 8>(g, p1.g, full, a1, st);
+    int rc = launch_tti_stream<R>(g, p1.g, full, a1, st);
     if (rc) return rc;
     UOp u{};
     u.out[0] = p.out[0];
     u.out[1] = p.out[1];
     u.k = p.c;
-    return R <= 4 ? launch_stream_op<R, 16>(u, p.g, full, a2, st)
-                  : launch_stream_op<R, 8>(u, p.g, full, a2, st);
+    return launch_tti_stream<R>(u, p.g, full, a2, st);
   }
   dim3 g1((p1.g.hi[2] - p1.g.lo[2] + 31) / 32, (p1.g.hi[1] - p1.g.lo[1] + 7) / 8,
           p1.g.hi[0] - p1.g.lo[0]);
