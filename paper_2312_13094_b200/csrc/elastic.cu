@@ -291,10 +291,12 @@ struct ViscoOp {
 template <int R, class Op>
 static int launch_el_stream(const Op& op, const Geom& g, const int64_t full[3],
                             const float* const* arrs, cudaStream_t st) {
-  constexpr bool big = Op::NP == 15;  // visco stress + memory variables
-  if constexpr (R <= 3) return launch_stream_op<R, 16, 2>(op, g, full, arrs, st);
-  else if constexpr (R == 4) return launch_stream_op<R, big ? 12 : 16, 2>(op, g, full, arrs, st);
-  else return launch_stream_op<R, 8, 2>(op, g, full, arrs, st);
+  // velocity (few operands, many taps) is issue bound: packed pairs; the
+  // stress phases (8-15 pointwise operands) are bandwidth bound: one point
+  // per thread keeps stages small and the ring deep (measured, r01).
+  constexpr int V = Op::NP <= 4 ? 2 : 1;
+  if constexpr (R <= 4) return launch_stream_op<R, 16, V>(op, g, full, arrs, st);
+  else return launch_stream_op<R, 8, V>(op, g, full, arrs, st);
 }
 
 // ---- host ----------------------------------------------------------------

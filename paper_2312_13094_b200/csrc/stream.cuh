@@ -44,7 +44,7 @@ struct SLayout {
   static constexpr int FRONT = TZ * TY * 4;
   static constexpr int CENTER = ((CZ * CY * 4) + 127) & ~127;
   static constexpr int STAGE = NF * FRONT + NC * CENTER + NP * FRONT;
-  static constexpr int S0 = (200 * 1024) / STAGE;
+  static constexpr int S0 = (220 * 1024) / STAGE;
   static constexpr int S = S0 > 4 ? 4 : (S0 < 2 ? 2 : S0);
   static constexpr int BYTES = S * STAGE + 2 * S * 8;
   static constexpr int THREADS = 32 * (TY + 1);
