@@ -396,6 +396,11 @@ class Action:
     region: str = ""
     event: int = -1
     sparse: object = None
+    # fused halo push (full mode): the compute / inject kernel also stores
+    # these output fields into the neighbours' HALO over NVLink:
+    # (output fields in kernel output order, messages giving the boxes)
+    push: Optional[tuple] = None
+    pushed: bool = False      # post: halos already pushed (copy only on run start)
 
 
 @dataclass
@@ -413,8 +418,67 @@ class ExecPlan:
         return sum(len(a.messages) for a in self.actions if a.kind == "post")
 
 
+def _fuse_pushes(acts, analysis: HaloAnalysis, decomp, rank: int) -> None:
+    """Full mode: fold the halo exchange into the kernels that produce the
+    OWNED values.  Every exchanged field's send boxes lie inside the OWNED
+    slabs (CORE is shrunk by the same radius), so the slab kernels (and the
+    source injection, which updates values after them) store every value a
+    neighbour needs straight into its HALO; the next post only releases the
+    flag (copies happen on the first step of a run, when nothing was
+    pushed).  Falls back to copies if any precondition fails."""
+    from .distfield import RegionName, diagonal_messages, rank_regions
+
+    radius = {}
+    for ph in analysis.phases:
+        if ph.halo is not None:
+            for f, _t in ph.halo.fields:
+                radius[f] = ph.halo.radius
+    if not radius:
+        return
+    geo = {f: diagonal_messages(decomp, rank, r) for f, r in radius.items()}
+    if any(len(m) > 8 for m in geo.values()):
+        return  # push lists hold 8 directions (x/y splits)
+
+    def outputs(k):
+        outs = [f for f, t in k.writes() if t == 1]
+        pushed = [f for f in outs if f in radius]
+        # the kernels push a PREFIX of their outputs with one geometry
+        if not pushed or outs[:len(pushed)] != pushed:
+            return None
+        if len({radius[f] for f in pushed}) != 1:
+            return None
+        return pushed
+
+    plan = []
+    for a in acts:
+        if a.kind == "compute" and a.region == "OWNED":
+            outs = outputs(a.kernel)
+            if outs is None:
+                if any(f in radius for f, _t in a.kernel.writes()):
+                    return
+                continue
+            plan.append((a, (outs, geo[outs[0]])))
+        elif a.kind == "compute" and a.region == "CORE":
+            # CORE must not intersect any pushed send box
+            outs = outputs(a.kernel) or []
+            for f in outs:
+                for m in geo[f]:
+                    lo = [max(x, y) for x, y in zip(a.box[0], m.send[0])]
+                    hi = [min(x, y) for x, y in zip(a.box[1], m.send[1])]
+                    if all(h > l for l, h in zip(lo, hi)):
+                        return
+        elif a.kind == "inject" and a.sparse.field in radius:
+            plan.append((a, ([a.sparse.field], geo[a.sparse.field])))
+    for a, push in plan:
+        a.push = push
+    for a in acts:
+        if a.kind == "post":
+            a.pushed = True
+
+
 def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
-               sparse_terms: Sequence = (), exchange: bool = True) -> ExecPlan:
+               sparse_terms: Sequence = (), exchange: bool = True,
+               fused: bool = True) -> ExecPlan:
     """Per-rank ExecPlan for ``mode``.
 
     ``exchange=False`` keeps the mode's compute boxes and stream structure
@@ -494,6 +558,8 @@ def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
         raise CompilerError("too many stream joins per step")
     if not exchange:
         acts = [a for a in acts if a.kind not in ("post", "wait")]
+    elif mode == "full" and fused:
+        _fuse_pushes(acts, analysis, decomp, rank)
     # phases per step is identical on every rank (epoch numbering)
     per_step = 0
     for ph in analysis.phases:

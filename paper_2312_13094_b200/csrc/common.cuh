@@ -63,6 +63,42 @@ inline int make_geom(const int64_t full[3], const int64_t lo[3], const int64_t h
   return SDMP_OK;
 }
 
+// ---- fused halo push (full mode) -------------------------------------------
+// A kernel that computes OWNED points also stores each result straight into
+// the HALO of every neighbour whose receive box contains it (IPC-mapped peer
+// pointers over NVLink): compute and halo exchange in ONE kernel.  For
+// direction d, points of [lo, hi) (this rank's FULL coordinates) land at
+// (x, y, z) + off in the peer's FULL array with strides (psx, psy, 1).
+constexpr int kPushDirs = 8;
+constexpr int kPushOut = 12;
+struct PushGeo {
+  int lo[3], hi[3], off[3];
+  int64_t psx, psy;
+};
+struct Push {
+  int ndir = 0, nout = 0;
+  int64_t msx = 0, msy = 0;  // this rank's strides (inject decodes node indices)
+  PushGeo geo[kPushDirs];
+  float* base[kPushOut][kPushDirs];
+};
+
+__device__ __forceinline__ bool push_in(const PushGeo& g, int x, int y, int z) {
+  return x >= g.lo[0] && x < g.hi[0] && y >= g.lo[1] && y < g.hi[1] && z >= g.lo[2] &&
+         z < g.hi[2];
+}
+
+// one point, `nv` outputs (vals[q] -> base[q])
+__device__ __forceinline__ void push_point(const Push& P, int x, int y, int z, const float* vals,
+                                           int nv) {
+  for (int d = 0; d < P.ndir; ++d) {
+    const PushGeo& g = P.geo[d];
+    if (!push_in(g, x, y, z)) continue;
+    const int64_t j = (int64_t)(x + g.off[0]) * g.psx + (int64_t)(y + g.off[1]) * g.psy +
+                      (z + g.off[2]);
+    for (int q = 0; q < nv && q < P.nout; ++q) P.base[q][d][j] = vals[q];
+  }
+}
+
 inline bool box_empty(const Geom& g) {
   return g.hi[0] <= g.lo[0] || g.hi[1] <= g.lo[1] || g.hi[2] <= g.lo[2];
 }

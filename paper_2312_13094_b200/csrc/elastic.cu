@@ -174,26 +174,28 @@ struct ElGeneric {
   GlobalAcc a{p.tap, p.pnt, i, {p.g.sx, p.g.sy, 1}};
 
 template <int R>
-__global__ void __launch_bounds__(256) el_velocity(ElGeneric p) {
+__global__ void __launch_bounds__(256) el_velocity(ElGeneric p, const Push push) {
   EL_INDEX
   float o[3];
   vel_point<R>(a, p.k, o);
   p.out[0][i] = o[0];
   p.out[1][i] = o[1];
   p.out[2][i] = o[2];
+  if (push.ndir) push_point(push, x, y, z, o, 3);
 }
 
 template <int R>
-__global__ void __launch_bounds__(256) el_stress(ElGeneric p) {
+__global__ void __launch_bounds__(256) el_stress(ElGeneric p, const Push push) {
   EL_INDEX
   float o[6];
   stress_point<R>(a, p.k, o);
 #pragma unroll
   for (int c = 0; c < 6; ++c) p.out[c][i] = o[c];
+  if (push.ndir) push_point(push, x, y, z, o, 6);
 }
 
 template <int R>
-__global__ void __launch_bounds__(256) visco_stress(ElGeneric p) {
+__global__ void __launch_bounds__(256) visco_stress(ElGeneric p, const Push push) {
   EL_INDEX
   float s1[6], r1[6];
   visco_point<R>(a, p.k, s1, r1);
@@ -202,6 +204,7 @@ __global__ void __launch_bounds__(256) visco_stress(ElGeneric p) {
     p.out[c][i] = s1[c];
     p.out[6 + c][i] = r1[c];
   }
+  if (push.ndir) push_point(push, x, y, z, s1, 6);  // memory variables stay local
 }
 
 // ---- stream operators ------------------------------------------------------
@@ -316,10 +319,11 @@ static int fill(ElGeneric& p, const int64_t full[3], const int64_t lo[3], const 
 }
 
 template <class K>
-static int launch_generic(const Geom& g, K kernel, const ElGeneric& params, cudaStream_t st) {
+static int launch_generic(const Geom& g, K kernel, const ElGeneric& params, cudaStream_t st,
+                          const Push& push) {
   dim3 b(32, 8);
   dim3 grid((g.hi[2] - g.lo[2] + 31) / 32, (g.hi[1] - g.lo[1] + 7) / 8, g.hi[0] - g.lo[0]);
-  kernel<<<grid, b, 0, st>>>(params);
+  kernel<<<grid, b, 0, st>>>(params, push);
   SDMP_LAUNCHED();
   return SDMP_OK;
 }
@@ -350,15 +354,13 @@ static int variant_env() {
   set_error("unsupported radius");                                             \
   return SDMP_EUNSUPPORTED;
 
-}  // namespace sdmp
-
-using namespace sdmp;
-
-extern "C" int sdmp_elastic_velocity(void* stream, const float* const v0[3],
+int elastic_velocity_impl(void* stream, const float* const v0[3],
                                      const float* const tau[6], const float* b,
                                      float* const v1[3], const int64_t full[3],
                                      const int64_t lo[3], const int64_t hi[3], int32_t radius,
-                                     const float* sc, float dt) {
+                                     const float* sc, float dt, const Push* push_in) {
+  const Push nopush{};
+  const Push& push = push_in ? *push_in : nopush;
   ElGeneric p{};
   int rc = fill(p, full, lo, hi, radius, sc, dt);
   if (rc) return rc;
@@ -370,21 +372,24 @@ extern "C" int sdmp_elastic_velocity(void* stream, const float* const v0[3],
   cudaStream_t st = (cudaStream_t)stream;
   const float* arrs[12] = {tau[0], tau[3], tau[4], tau[1], tau[2], tau[3], tau[4], tau[5],
                            v0[0], v0[1], v0[2], b};
-  if (variant_env() != 1 && stream_worth(p.g, radius) && stream_fits(p.g, radius) &&
+  if (variant_env() != 1 && push.ndir == 0 && stream_worth(p.g, radius) &&
+      stream_fits(p.g, radius) &&
       tma_ok(full, arrs, 12)) {
     VelOp op{};
     for (int c = 0; c < 3; ++c) op.out[c] = v1[c];
     op.k = p.k;
     RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st))
   }
-  RADIUS_SWITCH(launch_generic(p.g, el_velocity<RR>, p, st))
+  RADIUS_SWITCH(launch_generic(p.g, el_velocity<RR>, p, st, push))
 }
 
-extern "C" int sdmp_elastic_stress(void* stream, const float* const v1[3],
+int elastic_stress_impl(void* stream, const float* const v1[3],
                                    const float* const t0[6], const float* lam, const float* mu,
                                    float* const t1[6], const int64_t full[3],
                                    const int64_t lo[3], const int64_t hi[3], int32_t radius,
-                                   const float* sc, float dt) {
+                                   const float* sc, float dt, const Push* push_in) {
+  const Push nopush{};
+  const Push& push = push_in ? *push_in : nopush;
   ElGeneric p{};
   int rc = fill(p, full, lo, hi, radius, sc, dt);
   if (rc) return rc;
@@ -397,22 +402,25 @@ extern "C" int sdmp_elastic_stress(void* stream, const float* const v1[3],
   cudaStream_t st = (cudaStream_t)stream;
   const float* arrs[14] = {v1[0], v1[1], v1[2], v1[0], v1[1], v1[2],
                            t0[0], t0[1], t0[2], t0[3], t0[4], t0[5], lam, mu};
-  if (variant_env() != 1 && stream_worth(p.g, radius) && stream_fits(p.g, radius) &&
+  if (variant_env() != 1 && push.ndir == 0 && stream_worth(p.g, radius) &&
+      stream_fits(p.g, radius) &&
       tma_ok(full, arrs, 14)) {
     StressOp op{};
     for (int c = 0; c < 6; ++c) op.out[c] = t1[c];
     op.k = p.k;
     RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st))
   }
-  RADIUS_SWITCH(launch_generic(p.g, el_stress<RR>, p, st))
+  RADIUS_SWITCH(launch_generic(p.g, el_stress<RR>, p, st, push))
 }
 
-extern "C" int sdmp_visco_stress(void* stream, const float* const v1[3],
+int visco_stress_impl(void* stream, const float* const v1[3],
                                  const float* const s0[6], const float* const r0[6],
                                  const float* const prm[3], float* const s1[6],
                                  float* const r1[6], const int64_t full[3], const int64_t lo[3],
                                  const int64_t hi[3], int32_t radius, const float* sc,
-                                 float dt) {
+                                 float dt, const Push* push_in) {
+  const Push nopush{};
+  const Push& push = push_in ? *push_in : nopush;
   ElGeneric p{};
   int rc = fill(p, full, lo, hi, radius, sc, dt);
   if (rc) return rc;
@@ -431,12 +439,43 @@ extern "C" int sdmp_visco_stress(void* stream, const float* const v1[3],
   const float* arrs[21] = {v1[0], v1[1], v1[2], v1[0], v1[1], v1[2],
                            s0[0], s0[1], s0[2], s0[3], s0[4], s0[5],
                            r0[0], r0[1], r0[2], r0[3], r0[4], r0[5], prm[0], prm[1], prm[2]};
-  if (variant_env() != 1 && stream_worth(p.g, radius) && stream_fits(p.g, radius) &&
+  if (variant_env() != 1 && push.ndir == 0 && stream_worth(p.g, radius) &&
+      stream_fits(p.g, radius) &&
       tma_ok(full, arrs, 21)) {
     ViscoOp op{};
     for (int c = 0; c < 12; ++c) op.out[c] = p.out[c];
     op.k = p.k;
     RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st))
   }
-  RADIUS_SWITCH(launch_generic(p.g, visco_stress<RR>, p, st))
+  RADIUS_SWITCH(launch_generic(p.g, visco_stress<RR>, p, st, push))
+}
+
+}  // namespace sdmp
+
+using namespace sdmp;
+
+extern "C" int sdmp_elastic_velocity(void* stream, const float* const v0[3],
+                                     const float* const tau[6], const float* b,
+                                     float* const v1[3], const int64_t full[3],
+                                     const int64_t lo[3], const int64_t hi[3], int32_t radius,
+                                     const float* sc, float dt) {
+  return elastic_velocity_impl(stream, v0, tau, b, v1, full, lo, hi, radius, sc, dt, nullptr);
+}
+
+extern "C" int sdmp_elastic_stress(void* stream, const float* const v1[3],
+                                   const float* const t0[6], const float* lam, const float* mu,
+                                   float* const t1[6], const int64_t full[3],
+                                   const int64_t lo[3], const int64_t hi[3], int32_t radius,
+                                   const float* sc, float dt) {
+  return elastic_stress_impl(stream, v1, t0, lam, mu, t1, full, lo, hi, radius, sc, dt, nullptr);
+}
+
+extern "C" int sdmp_visco_stress(void* stream, const float* const v1[3],
+                                 const float* const s0[6], const float* const r0[6],
+                                 const float* const prm[3], float* const s1[6],
+                                 float* const r1[6], const int64_t full[3], const int64_t lo[3],
+                                 const int64_t hi[3], int32_t radius, const float* sc,
+                                 float dt) {
+  return visco_stress_impl(stream, v1, s0, r0, prm, s1, r1, full, lo, hi, radius, sc, dt,
+                           nullptr);
 }

@@ -32,11 +32,23 @@ const char* get_error() { return g_err.c_str(); }
 
 int star_update(cudaStream_t, const float*, const float*, const float*, float*, const int64_t*,
                 const int64_t*, const int64_t*, const int32_t*, const float*, float, float, float,
-                int);
+                int, const Push*);
 int tti_update_entry(cudaStream_t, const float* const*, float*, float*, const int64_t*,
-                     const int64_t*, const int64_t*, int32_t, const float*, const float*, float);
+                     const int64_t*, const int64_t*, int32_t, const float*, const float*, float,
+                     const Push*);
 int inject(cudaStream_t, float*, const int64_t*, const int32_t*, int, const int32_t*,
-           const float*, const float*, float, const float*, const int64_t*, int64_t, int64_t);
+           const float*, const float*, float, const float*, const int64_t*, int64_t, int64_t,
+           const Push*);
+int elastic_velocity_impl(void*, const float* const[3], const float* const[6], const float*,
+                          float* const[3], const int64_t[3], const int64_t[3], const int64_t[3],
+                          int32_t, const float*, float, const Push*);
+int elastic_stress_impl(void*, const float* const[3], const float* const[6], const float*,
+                        const float*, float* const[6], const int64_t[3], const int64_t[3],
+                        const int64_t[3], int32_t, const float*, float, const Push*);
+int visco_stress_impl(void*, const float* const[3], const float* const[6],
+                      const float* const[6], const float* const[3], float* const[6],
+                      float* const[6], const int64_t[3], const int64_t[3], const int64_t[3],
+                      int32_t, const float*, float, const Push*);
 int interpolate(cudaStream_t, const float*, const int64_t*, const float*, int, int, float*,
                 const int64_t*, int64_t, int64_t);
 int set_ctr(cudaStream_t, int64_t*, int64_t, int64_t);
@@ -48,19 +60,6 @@ int wait_flags(cudaStream_t, uint32_t* const*, int, uint32_t, unsigned long long
                const int64_t*, int, int);
 
 }  // namespace sdmp
-
-extern "C" int sdmp_elastic_velocity(void*, const float* const[3], const float* const[6],
-                                     const float*, float* const[3], const int64_t[3],
-                                     const int64_t[3], const int64_t[3], int32_t, const float*,
-                                     float);
-extern "C" int sdmp_elastic_stress(void*, const float* const[3], const float* const[6],
-                                   const float*, const float*, float* const[6], const int64_t[3],
-                                   const int64_t[3], const int64_t[3], int32_t, const float*,
-                                   float);
-extern "C" int sdmp_visco_stress(void*, const float* const[3], const float* const[6],
-                                 const float* const[6], const float* const[3], float* const[6],
-                                 float* const[6], const int64_t[3], const int64_t[3],
-                                 const int64_t[3], int32_t, const float*, float);
 
 using namespace sdmp;
 
@@ -108,6 +107,7 @@ struct sdmp_plan {
   std::vector<SparseSet> sparse;
   std::vector<Action> actions;
   int64_t steps_done = 0;
+  int64_t run_time_m = 0;  // first timestep of the current run
   // device step counter {time, steps_done}: sparse rows and exchange epochs
   // are read from it so a captured period of steps can be replayed
   int64_t* dev_ctr = nullptr;
@@ -132,6 +132,59 @@ float* resolve(const sdmp_plan* p, int64_t f, int64_t t, int64_t time) {
   return reinterpret_cast<float*>(fl.ptr[b]);
 }
 
+// Optional fused-push block appended to a compute / inject action:
+// [kPushMagic, ndir, nout, tshift, ndir x (lo3, hi3, off3), nout x ndir peer
+// field ids (output-major)].  Peer buffers are resolved for this timestep.
+constexpr int64_t kPushMagic = -77;
+
+int base_len(int kind) {
+  switch (kind) {
+    case SDMP_ACT_STAR: return 19;
+    case SDMP_ACT_TTI: return 33;
+    case SDMP_ACT_EL_V: return 35;
+    case SDMP_ACT_EL_T: return 43;
+    case SDMP_ACT_VISCO_T: return 69;
+    case SDMP_ACT_INJECT: return 6;
+    default: return -1;
+  }
+}
+
+// returns 1 if a push block was decoded into *out, 0 if none, < 0 on error
+int parse_push(const sdmp_plan* p, const Action& a, int64_t time, Push* out) {
+  const int b = base_len((int)a.i[0]);
+  if (b < 0 || (int64_t)a.i.size() <= b || a.i[b] != kPushMagic) return 0;
+  const int64_t* I = a.i.data() + b;
+  const int ndir = (int)I[1], nout = (int)I[2];
+  const int64_t tsh = I[3];
+  SDMP_CHECK(ndir >= 0 && ndir <= kPushDirs && nout >= 1 && nout <= kPushOut, "push sizes");
+  SDMP_CHECK((int64_t)a.i.size() >= b + 4 + 9 * ndir + nout * ndir, "push block truncated");
+  out->ndir = ndir;
+  out->nout = nout;
+  const int64_t* gp = I + 4;
+  const int64_t* fid = I + 4 + 9 * ndir;
+  for (int d = 0; d < ndir; ++d) {
+    PushGeo& g = out->geo[d];
+    for (int k = 0; k < 3; ++k) {
+      g.lo[k] = (int)gp[9 * d + k];
+      g.hi[k] = (int)gp[9 * d + 3 + k];
+      g.off[k] = (int)gp[9 * d + 6 + k];
+    }
+    const int64_t pf = fid[d];  // output 0 of direction d
+    SDMP_CHECK(pf >= 0 && pf < (int64_t)p->fields.size(), "push field id");
+    g.psy = p->fields[pf].full[2];
+    g.psx = p->fields[pf].full[1] * p->fields[pf].full[2];
+    for (int q = 0; q < nout; ++q) {
+      const int64_t f = fid[q * ndir + d];
+      SDMP_CHECK(f >= 0 && f < (int64_t)p->fields.size(), "push field id");
+      out->base[q][d] = resolve(p, f, tsh, time);
+    }
+  }
+  const int64_t lf = a.i[2];  // first field of the action: this rank's layout
+  out->msy = p->fields[lf].full[2];
+  out->msx = p->fields[lf].full[1] * p->fields[lf].full[2];
+  return 1;
+}
+
 // Kernel launches one action issues per step (copy-engine copies are not
 // kernel launches).
 int launches_of(const Action& a) {
@@ -153,6 +206,10 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
   const float* F = a.f.data();
   const int kind = (int)I[0];
   cudaStream_t st = p->s[I[1]];
+  Push push;
+  const int hp = parse_push(p, a, time, &push);
+  if (hp < 0) return hp;
+  const Push* pp = hp ? &push : nullptr;
   switch (kind) {
     case SDMP_ACT_STAR: {
       // [k,s, fu0,tu0, fu2,tu2, fm, fu1,tu1, lo3, hi3, r3, variant]
@@ -165,7 +222,7 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       int32_t r[3] = {(int32_t)I[15], (int32_t)I[16], (int32_t)I[17]};
       const int nc = 3 * SDMP_NCOEF;
       return star_update(st, u0, u2, m, u1, p->fields[I[2]].full, lo, hi, r, F, F[nc],
-                         F[nc + 1], F[nc + 2], (int)I[18]);
+                         F[nc + 1], F[nc + 2], (int)I[18], pp);
     }
     case SDMP_ACT_TTI: {
       const float* in[10];
@@ -176,7 +233,7 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       const int64_t* hi = I + 29;
       const int nc = 3 * SDMP_NCOEF;
       return tti_update_entry(st, in, p1, r1, p->fields[I[2]].full, lo, hi, (int32_t)I[32], F,
-                              F + nc, F[2 * nc]);
+                              F + nc, F[2 * nc], pp);
     }
     case SDMP_ACT_EL_V: {
       const float* v0[3]; const float* tau[6]; float* v1[3];
@@ -186,8 +243,8 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       for (int k = 0; k < 3; ++k) v1[k] = resolve(p, I[22 + 2 * k], I[23 + 2 * k], time);
       const int64_t* lo = I + 28;
       const int64_t* hi = I + 31;
-      return sdmp_elastic_velocity(st, v0, tau, b, v1, p->fields[I[2]].full, lo, hi,
-                                   (int32_t)I[34], F, F[3 * SDMP_MAX_RADIUS]);
+      return elastic_velocity_impl(st, v0, tau, b, v1, p->fields[I[2]].full, lo, hi,
+                                   (int32_t)I[34], F, F[3 * SDMP_MAX_RADIUS], pp);
     }
     case SDMP_ACT_EL_T: {
       const float* v1[3]; const float* t0[6]; float* t1[6];
@@ -198,8 +255,8 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       for (int k = 0; k < 6; ++k) t1[k] = resolve(p, I[24 + 2 * k], I[25 + 2 * k], time);
       const int64_t* lo = I + 36;
       const int64_t* hi = I + 39;
-      return sdmp_elastic_stress(st, v1, t0, lam, mu, t1, p->fields[I[2]].full, lo, hi,
-                                 (int32_t)I[42], F, F[3 * SDMP_MAX_RADIUS]);
+      return elastic_stress_impl(st, v1, t0, lam, mu, t1, p->fields[I[2]].full, lo, hi,
+                                 (int32_t)I[42], F, F[3 * SDMP_MAX_RADIUS], pp);
     }
     case SDMP_ACT_VISCO_T: {
       const float* v1[3]; const float* s0[6]; const float* r0[6]; const float* prm[3];
@@ -213,8 +270,8 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       for (int k = 0; k < 6; ++k, o += 2) r1[k] = resolve(p, I[o], I[o + 1], time);
       const int64_t* lo = I + o;
       const int64_t* hi = I + o + 3;
-      return sdmp_visco_stress(st, v1, s0, r0, prm, s1, r1, p->fields[I[2]].full, lo, hi,
-                               (int32_t)I[o + 6], F, F[3 * SDMP_MAX_RADIUS]);
+      return visco_stress_impl(st, v1, s0, r0, prm, s1, r1, p->fields[I[2]].full, lo, hi,
+                               (int32_t)I[o + 6], F, F[3 * SDMP_MAX_RADIUS], pp);
     }
     case SDMP_ACT_INJECT: {
       // [k,s, ffield,t, fm, set]
@@ -223,7 +280,7 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       const SparseSet& ss = p->sparse[I[5]];
       if (time < ss.t0) return SDMP_OK;
       return inject(st, fld, ss.node, ss.ptr, ss.nnodes, ss.pid, ss.w, ss.series, F[0], m,
-                    p->dev_ctr, ss.stride, ss.t0);
+                    p->dev_ctr, ss.stride, ss.t0, pp);
     }
     case SDMP_ACT_INTERP: {
       const float* fld = resolve(p, I[2], I[3], time);
@@ -234,8 +291,13 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
     }
     case SDMP_ACT_POST: {
       // [k,s, phase, nmsg, engine, msgs(12 each: fsrc,t,fdst,slo3,dlo3,ext3)..., nsig, (flags_id, slot)...]
-      const int64_t phase = I[2], nmsg = I[3];
-      const int engine = (int)I[4];
+      // I[4]: bit 0 engine (0 copy engine, 1 SM stores); bit 4: halos were
+      // already pushed by the fused compute kernels, copy only on the first
+      // step of a run (nothing was pushed before it)
+      const int64_t phase = I[2];
+      const int engine = (int)(I[4] & 1);
+      const bool pushed = (I[4] & 16) && time != p->run_time_m;
+      const int64_t nmsg = pushed ? 0 : I[3];
       const int64_t* m = I + 5;
       const int fan = (engine == 0 && nmsg > 1) ? (int)(nmsg < sdmp_plan::kCopy ? nmsg
                                                                               : sdmp_plan::kCopy)
@@ -258,6 +320,7 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
           SDMP_CUDA(cudaStreamWaitEvent(st, p->ev_cdone[c], 0));
         }
       }
+      if (pushed) m = I + 5 + 12 * I[3];
       const int64_t nsig = *m++;
       uint32_t* ptrs[32];
       SDMP_CHECK(nsig <= 32, "too many signals");
@@ -662,13 +725,14 @@ extern "C" int sdmp_plan_run(sdmp_plan* p, int64_t time_m, int64_t time_M, void*
   SDMP_CUDA(cudaStreamWaitEvent(p->s[0], p->ev_in, 0));
   int rc = set_ctr(p->s[0], p->dev_ctr, time_m, p->steps_done);
   if (rc) return rc;
+  p->run_time_m = time_m;
   int64_t time = time_m;
   // graphs: only after the plan has run once (lazy attributes, scratch
   // allocations and TMA descriptor entry points are resolved by then)
   const bool graphs = p->graph_on && !p->tracing && p->period >= 1 && p->steps_done > 0;
   while (time <= time_M) {
     const int64_t left = time_M - time + 1;
-    if (graphs && left >= p->period) {
+    if (graphs && time > time_m && left >= p->period) {
       const int64_t r = ((time % p->period) + p->period) % p->period;
       auto it = p->graphs.find(r);
       if (it == p->graphs.end()) {

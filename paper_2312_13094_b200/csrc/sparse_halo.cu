@@ -16,7 +16,8 @@ __global__ void k_inject(float* __restrict__ f, const int64_t* __restrict__ node
                          const int32_t* __restrict__ ptr, int nnodes,
                          const int32_t* __restrict__ pid, const float* __restrict__ w,
                          const float* __restrict__ amps, float C, const float* __restrict__ m,
-                         const int64_t* __restrict__ ctr, int64_t stride, int64_t t0) {
+                         const int64_t* __restrict__ ctr, int64_t stride, int64_t t0,
+                         const Push push) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= nnodes) return;
   if (ctr) amps += (ctr[0] - t0) * stride;
@@ -24,7 +25,15 @@ __global__ void k_inject(float* __restrict__ f, const int64_t* __restrict__ node
   for (int j = ptr[n]; j < ptr[n + 1]; ++j) acc = __fmaf_rn(w[j], amps[pid[j]], acc);
   const int64_t i = node[n];
   const float s = m ? __fdiv_rn(C, m[i]) : C;
-  f[i] = __fmaf_rn(acc, s, f[i]);
+  const float v = __fmaf_rn(acc, s, f[i]);
+  f[i] = v;
+  if (push.ndir) {  // full mode: the injected value also reaches the peers' halos
+    const int x = (int)(i / push.msx);
+    const int64_t rem = i - (int64_t)x * push.msx;
+    const int y = (int)(rem / push.msy);
+    const int z = (int)(rem - (int64_t)y * push.msy);
+    push_point(push, x, y, z, &v, 1);
+  }
 }
 
 __global__ void k_interp(const float* __restrict__ f, const int64_t* __restrict__ idx,
@@ -40,11 +49,12 @@ __global__ void k_interp(const float* __restrict__ f, const int64_t* __restrict_
 
 int inject(cudaStream_t st, float* field, const int64_t* node, const int32_t* ptr, int nnodes,
            const int32_t* pid, const float* w, const float* amps, float C, const float* m,
-           const int64_t* ctr, int64_t stride, int64_t t0) {
+           const int64_t* ctr, int64_t stride, int64_t t0, const Push* push) {
   if (nnodes <= 0) return SDMP_OK;
   SDMP_CHECK(field && node && ptr && pid && w && amps, "inject: null array");
+  const Push nopush{};
   k_inject<<<(nnodes + 127) / 128, 128, 0, st>>>(field, node, ptr, nnodes, pid, w, amps, C, m,
-                                                 ctr, stride, t0);
+                                                 ctr, stride, t0, push ? *push : nopush);
   SDMP_LAUNCHED();
   return SDMP_OK;
 }
@@ -288,7 +298,7 @@ extern "C" int sdmp_inject(void* stream, float* field, const int64_t* node, cons
                            int32_t nnodes, const int32_t* pid, const float* w,
                            const float* amps, float C, const float* m) {
   return inject((cudaStream_t)stream, field, node, ptr, nnodes, pid, w, amps, C, m, nullptr, 0,
-                0);
+                0, nullptr);
 }
 
 extern "C" int sdmp_interpolate(void* stream, const float* field, const int64_t* idx,

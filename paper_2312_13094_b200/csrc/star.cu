@@ -68,7 +68,7 @@ __device__ __forceinline__ float star_point(const StarParams& p, float c0, float
 // ---------------------------------------------------------------------------
 // generic: one thread per point
 
-__global__ void __launch_bounds__(256) star_generic(StarParams p) {
+__global__ void __launch_bounds__(256) star_generic(StarParams p, const Push push) {
   const int z = p.g.lo[2] + blockIdx.x * 32 + threadIdx.x;
   const int y = p.g.lo[1] + blockIdx.y * 8 + threadIdx.y;
   const int x = p.g.lo[0] + blockIdx.z;
@@ -82,7 +82,9 @@ __global__ void __launch_bounds__(256) star_generic(StarParams p) {
   auto xs = [&](int k) { return __fadd_rn(__ldg(u + i - k * sx), __ldg(u + i + k * sx)); };
   auto ys = [&](int k) { return __fadd_rn(__ldg(u + i - k * sy), __ldg(u + i + k * sy)); };
   auto zs = [&](int k) { return __fadd_rn(__ldg(u + i - k), __ldg(u + i + k)); };
-  p.u1[i] = star_point<0, 0, 0>(p, c0, u2v, mv, p.r[0], p.r[1], p.r[2], xs, ys, zs);
+  const float v = star_point<0, 0, 0>(p, c0, u2v, mv, p.r[0], p.r[1], p.r[2], xs, ys, zs);
+  p.u1[i] = v;
+  if (push.ndir) push_point(push, x, y, z, &v, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -261,7 +263,7 @@ template <int R, int TY>
 __global__ void __launch_bounds__(TmaCfg<R, TY>::THREADS, 1)
 star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ CUtensorMap tm_center,
          const __grid_constant__ CUtensorMap tm_u2, const __grid_constant__ CUtensorMap tm_m,
-         StarParams p, int xchunk) {
+         StarParams p, int xchunk, const Push push) {
   using T = TmaCfg<R, TY>;
   // __align__(1024) keeps TMA destinations aligned without integer pointer
   // arithmetic, so the compiler still sees shared-space pointers (LDS, not
@@ -373,6 +375,23 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
         out[j] = star_finish(p, lap[j], f4get(w[R], j), f4get(u2v, j), f4get(mv, j));
       __stcs(reinterpret_cast<float4*>(p.u1 + (int64_t)x * sx + col),
              make_float4(out[0], out[1], out[2], out[3]));
+      // fused halo push: this float4 also lands in every neighbour HALO
+      // whose receive box contains it (x/y-split boxes span full z rows)
+      for (int d = 0; d < push.ndir; ++d) {
+        const PushGeo& pg = push.geo[d];
+        if (x < pg.lo[0] || x >= pg.hi[0] || y < pg.lo[1] || y >= pg.hi[1] ||
+            z + 3 < pg.lo[2] || z >= pg.hi[2])
+          continue;
+        float* dst = push.base[0][d] + (int64_t)(x + pg.off[0]) * pg.psx +
+                     (int64_t)(y + pg.off[1]) * pg.psy + (z + pg.off[2]);
+        if (z >= pg.lo[2] && z + 3 < pg.hi[2] && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+          *reinterpret_cast<float4*>(dst) = make_float4(out[0], out[1], out[2], out[3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (z + j >= pg.lo[2] && z + j < pg.hi[2]) dst[j] = out[j];
+        }
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
@@ -399,7 +418,8 @@ static int pick_chunks(int64_t tiles, int nx, int R, int ctas_per_sm) {
 }
 
 template <int R, int TY>
-static int launch_tma(const StarParams& p, cudaStream_t st, const int64_t full[3]) {
+static int launch_tma(const StarParams& p, cudaStream_t st, const int64_t full[3],
+                      const Push& push) {
   using T = TmaCfg<R, TY>;
   static int attr_dev = -1;
   int dev = 0;
@@ -422,17 +442,17 @@ static int launch_tma(const StarParams& p, cudaStream_t st, const int64_t full[3
   nch = (nx + chunk - 1) / chunk;
   SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");
   dim3 grid(tz, ty, nch), block(32, TY + 1);
-  star_tma<R, TY><<<grid, block, T::BYTES, st>>>(tf, tc, t2, tm, p, chunk);
+  star_tma<R, TY><<<grid, block, T::BYTES, st>>>(tf, tc, t2, tm, p, chunk, push);
   SDMP_LAUNCHED();
   return SDMP_OK;
 }
 
-static int launch_generic(const StarParams& p, cudaStream_t st) {
+static int launch_generic(const StarParams& p, cudaStream_t st, const Push& push) {
   const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
   SDMP_CHECK(nx <= 65535, "generic kernel: box x extent > 65535");
   dim3 block(32, 8);
   dim3 grid((nz + 31) / 32, (ny + 7) / 8, nx);
-  star_generic<<<grid, block, 0, st>>>(p);
+  star_generic<<<grid, block, 0, st>>>(p, push);
   SDMP_LAUNCHED();
   return SDMP_OK;
 }
@@ -440,7 +460,9 @@ static int launch_generic(const StarParams& p, cudaStream_t st) {
 int star_update(cudaStream_t st, const float* u0, const float* u2, const float* m, float* u1,
                 const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
                 const int32_t radius[3], const float* coeffs, float A, float B, float C,
-                int variant) {
+                int variant, const Push* push_in) {
+  const Push nopush{};
+  const Push& push = push_in ? *push_in : nopush;
   StarParams p;
   int rc = make_geom(full, lo, hi, &p.g);
   if (rc) return rc;
@@ -466,8 +488,8 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
                           (full[2] % 4 == 0) && (lo[2] % 4 == 0) && ((hi[2] - lo[2]) % 4 == 0) &&
                           (((uintptr_t)u0 | (uintptr_t)u1 | (uintptr_t)u2 | (uintptr_t)m) % 16 == 0);
   // unaligned / unequal-radius boxes always take the generic kernel
-  if (variant == 1 || !streamable) return launch_generic(p, st);
-  if (variant == 2) {
+  if (variant == 1 || !streamable) return launch_generic(p, st, push);
+  if (variant == 2 && push.ndir == 0) {  // baseline kernel: no fused push
     switch (R) {
       case 1: return launch_stream<1>(p, st);
       case 2: return launch_stream<2>(p, st);
@@ -480,16 +502,16 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
     }
   }
   switch (R) {  // variant 0 (auto) / 3: TMA pipeline
-    case 1: return launch_tma<1, 16>(p, st, full);
-    case 2: return launch_tma<2, 16>(p, st, full);
-    case 3: return launch_tma<3, 16>(p, st, full);
-    case 4: return launch_tma<4, 16>(p, st, full);
-    case 5: return launch_tma<5, 16>(p, st, full);
-    case 6: return launch_tma<6, 8>(p, st, full);
-    case 7: return launch_tma<7, 8>(p, st, full);
-    case 8: return launch_tma<8, 8>(p, st, full);
+    case 1: return launch_tma<1, 16>(p, st, full, push);
+    case 2: return launch_tma<2, 16>(p, st, full, push);
+    case 3: return launch_tma<3, 16>(p, st, full, push);
+    case 4: return launch_tma<4, 16>(p, st, full, push);
+    case 5: return launch_tma<5, 16>(p, st, full, push);
+    case 6: return launch_tma<6, 8>(p, st, full, push);
+    case 7: return launch_tma<7, 8>(p, st, full, push);
+    case 8: return launch_tma<8, 8>(p, st, full, push);
   }
-  return launch_generic(p, st);
+  return launch_generic(p, st, push);
 }
 
 }  // namespace sdmp
@@ -500,5 +522,5 @@ extern "C" int sdmp_star_update(void* stream, const float* u0, const float* u2, 
                                 const float* coeffs, float A, float B, float C,
                                 int32_t variant) {
   return sdmp::star_update((cudaStream_t)stream, u0, u2, m, u1, full, lo, hi, radius, coeffs,
-                           A, B, C, variant);
+                           A, B, C, variant, nullptr);
 }

@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) tti_g(TTIGeneric p) {
 }
 
 template <int R>
-__global__ void __launch_bounds__(256) tti_update(TTIGeneric p) {
+__global__ void __launch_bounds__(256) tti_update(TTIGeneric p, const Push push) {
   const int z = p.g.lo[2] + blockIdx.x * 32 + threadIdx.x;
   const int y = p.g.lo[1] + blockIdx.y * 8 + threadIdx.y;
   const int x = p.g.lo[0] + blockIdx.z;
@@ -159,6 +159,10 @@ __global__ void __launch_bounds__(256) tti_update(TTIGeneric p) {
   u_point<R>(a, p.c, p1, r1);
   p.out[0][i] = p1;
   p.out[1][i] = r1;
+  if (push.ndir) {
+    const float v[2] = {p1, r1};
+    push_point(push, x, y, z, v, 2);
+  }
 }
 
 // ---- stream operators --------------------------------------------------------
@@ -264,7 +268,7 @@ static int variant_env() {
 }
 
 template <int R>
-static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3]) {
+static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const Push& push) {
   // pass 1 on the box grown by R (g is read up to R away by pass 2)
   TTIGeneric p1 = p;
   for (int a = 0; a < 3; ++a) {
@@ -279,7 +283,8 @@ static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3]) {
                          p.tap[TAY], p.tap[TAZ], p.tap[TGP], p.tap[TGR], p.tap[TP],
                          p.pnt[QP2], p.pnt[QR0], p.pnt[QR2], p.pnt[QM], p.pnt[QE], p.pnt[QD]};
   const bool thick = (p.g.hi[0] - p.g.lo[0]) >= 4 * R && (p.g.hi[1] - p.g.lo[1]) >= 16;
-  const bool stream = variant_env() != 1 && thick && stream_fits(p1.g, R) && stream_fits(p.g, R) &&
+  const bool stream = variant_env() != 1 && push.ndir == 0 && thick && stream_fits(p1.g, R) &&
+                      stream_fits(p.g, R) &&
                       tma_ok(full, a1, 7) && tma_ok(full, a2, 15);
   dim3 b(32, 8);
   if (stream) {
@@ -301,14 +306,17 @@ static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3]) {
   SDMP_LAUNCHED();
   dim3 g2((p.g.hi[2] - p.g.lo[2] + 31) / 32, (p.g.hi[1] - p.g.lo[1] + 7) / 8,
           p.g.hi[0] - p.g.lo[0]);
-  tti_update<R><<<g2, b, 0, st>>>(p);
+  tti_update<R><<<g2, b, 0, st>>>(p, push);
   SDMP_LAUNCHED();
   return SDMP_OK;
 }
 
 int tti_update_entry(cudaStream_t st, const float* const in[10], float* p1, float* r1,
                      const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
-                     int32_t radius, const float* lap_c, const float* d1_c, float dt2) {
+                     int32_t radius, const float* lap_c, const float* d1_c, float dt2,
+                     const Push* push_in) {
+  const Push nopush{};
+  const Push& push = push_in ? *push_in : nopush;
   TTIGeneric p{};
   int rc = make_geom(full, lo, hi, &p.g);
   if (rc) return rc;
@@ -343,14 +351,14 @@ int tti_update_entry(cudaStream_t st, const float* const in[10], float* p1, floa
   p.c.csum0 = cs;
   p.c.dt2 = dt2;
   switch (radius) {
-    case 1: return launch<1>(p, st, full);
-    case 2: return launch<2>(p, st, full);
-    case 3: return launch<3>(p, st, full);
-    case 4: return launch<4>(p, st, full);
-    case 5: return launch<5>(p, st, full);
-    case 6: return launch<6>(p, st, full);
-    case 7: return launch<7>(p, st, full);
-    case 8: return launch<8>(p, st, full);
+    case 1: return launch<1>(p, st, full, push);
+    case 2: return launch<2>(p, st, full, push);
+    case 3: return launch<3>(p, st, full, push);
+    case 4: return launch<4>(p, st, full, push);
+    case 5: return launch<5>(p, st, full, push);
+    case 6: return launch<6>(p, st, full, push);
+    case 7: return launch<7>(p, st, full, push);
+    case 8: return launch<8>(p, st, full, push);
   }
   set_error("tti: unsupported radius");
   return SDMP_EUNSUPPORTED;
@@ -364,5 +372,5 @@ extern "C" int sdmp_tti_update(void* stream, const float* const in[10], float* p
                                int32_t variant) {
   (void)variant;
   return sdmp::tti_update_entry((cudaStream_t)stream, in, p1, r1, full, lo, hi, radius, lap_c,
-                                d1_c, dt2);
+                                d1_c, dt2, nullptr);
 }

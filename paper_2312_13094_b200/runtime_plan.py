@@ -182,7 +182,8 @@ class NativeOperatorPlan:
         # ExecPlan action -> index of its native action (-1: nothing to do)
         self.native_index.append(self.plan.nact)
         if a.kind == "compute":
-            P.add_action(*self._compute_ints(a.kernel, a.box, a.stream))
+            ints, fl = self._compute_ints(a.kernel, a.box, a.stream)
+            P.add_action(ints + self._push_ints(a), fl)
         elif a.kind == "post":
             if not a.messages:
                 self.native_index[-1] = -1
@@ -200,13 +201,37 @@ class NativeOperatorPlan:
             P.add_action([R.ACT["STREAMWAIT"], a.stream, a.event])
         elif a.kind == "inject":
             sid, mid, C = self.sparse_sets[id(a.sparse)][:3]
-            P.add_action([R.ACT["INJECT"], a.stream, self.fid[a.sparse.field], 1, mid, sid], [C])
+            P.add_action([R.ACT["INJECT"], a.stream, self.fid[a.sparse.field], 1, mid, sid]
+                         + self._push_ints(a), [C])
         elif a.kind == "interp":
             sid = self.sparse_sets[id(a.sparse)][0]
             P.add_action([R.ACT["INTERP"], a.stream, self.fid[a.sparse.field], 0, sid])
 
+    PUSH_MAGIC = -77
+
+    def _push_ints(self, a) -> list:
+        """Fused-push block (csrc/plan.cu parse_push): each output value of
+        the action inside a send box is also stored into the neighbour's
+        HALO (same buffer rotation, tshift +1)."""
+        if a.push is None:
+            return []
+        outs, msgs = a.push
+        fn = self.op.fields[outs[0]]
+        h = fn.halo3
+        nd = len(msgs[0].send[0]) if msgs else 3
+        ints = [self.PUSH_MAGIC, len(msgs), len(outs), 1]
+        for m in msgs:
+            lo = [l + hh for l, hh in zip(m.send[0], h)] + [0] * (3 - nd)
+            hi = [u + hh for u, hh in zip(m.send[1], h)] + [1] * (3 - nd)
+            off = [r - s_ for r, s_ in zip(m.recv[0], m.send[0])] + [0] * (3 - nd)
+            ints += lo + hi + off
+        for f in outs:
+            for m in msgs:
+                ints.append(self.pfid[(m.peer, f)])
+        return ints
+
     def _post_ints(self, a, fid, pfid, pflag, decomp, rank):
-        ints = [R.ACT["POST"], a.stream, a.phase, 0, 0]
+        ints = [R.ACT["POST"], a.stream, a.phase, 0, 16 if a.pushed else 0]
         n = 0
         for m in a.messages:
             for f, t in a.spot.fields:
