@@ -523,8 +523,9 @@ class Operator:
         """The per-rank ExecPlan (host description; used by tests)."""
         mode = CP.normalise_mode(mode or _env_mode())
         an = CP.halo_phases(self.kernels, self.grid.decomposition.nranks)
+        fused = os.environ.get("SDMP_FUSED", "1") != "0"
         return CP.lower_mode(an, self.grid.decomposition, self.grid.rank, mode,
-                             self.sparse_terms, exchange=exchange)
+                             self.sparse_terms, exchange=exchange, fused=fused)
 
     def _native(self, mode, dt, exchange=True):
         key = (mode, None if dt is None else float(np.float32(dt)), exchange)
