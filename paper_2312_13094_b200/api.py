@@ -500,6 +500,7 @@ class Operator:
                 kernel_like.append(e)
             else:
                 kernel_like.append(_as_update(e))
+        self.updates = [e for e in kernel_like if isinstance(e, S.StencilEquation)]
         self.kernels = CP.recognise(kernel_like)
         self.fields: Dict[S.FieldSpec, Function] = {}
         for k in self.kernels:
@@ -526,6 +527,11 @@ class Operator:
         fused = os.environ.get("SDMP_FUSED", "1") != "0"
         return CP.lower_mode(an, self.grid.decomposition, self.grid.rank, mode,
                              self.sparse_terms, exchange=exchange, fused=fused)
+
+    def dump(self, mode=None) -> str:
+        """Listing 6/7-style plan text (HaloSpots, or the mode's update /
+        wait calls around the CORE / REMAINDER loop nests)."""
+        return CP.dump_plan(self.kernels, self.grid.decomposition.nranks, mode, self.updates)
 
     def _native(self, mode, dt, exchange=True):
         key = (mode, None if dt is None else float(np.float32(dt)), exchange)

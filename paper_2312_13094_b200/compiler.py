@@ -313,6 +313,32 @@ def recognise(equations: Sequence) -> List[object]:
 
 
 # ---------------------------------------------------------------------------
+# Access alignment
+
+
+def align_accesses(eq: S.StencilEquation, halo=None) -> S.StencilEquation:
+    """Shift every spatial index by +halo (``u[t,x,y]`` -> ``u[t,x+2,y+2]``
+    for SO-2).  ``halo`` = per-axis width for all fields, or None for each
+    field's own halo.  Relative offsets are unchanged."""
+
+    def move(n):
+        if isinstance(n, S.FieldAccess):
+            h = n.spec.halo if halo is None else tuple(halo)
+            return S.FieldAccess(n.spec, n.tshift, tuple(o + k for o, k in zip(n.offsets, h)))
+        return n
+
+    lhs = move(eq.lhs)
+    rhs = S.transform(eq.rhs, move)
+    temps = tuple((name, S.transform(body, move)) for name, body in eq.temporaries)
+    # bypass the explicit-scheme check (already validated on the input)
+    out = object.__new__(S.StencilEquation)
+    object.__setattr__(out, "lhs", lhs)
+    object.__setattr__(out, "rhs", rhs)
+    object.__setattr__(out, "temporaries", temps)
+    return out
+
+
+# ---------------------------------------------------------------------------
 # HaloSpots
 
 
@@ -416,6 +442,64 @@ class ExecPlan:
 
     def message_count(self) -> int:
         return sum(len(a.messages) for a in self.actions if a.kind == "post")
+
+
+def optimize_halospots(kernels: Sequence, nranks: int) -> HaloAnalysis:
+    """SPEC.md:348-356 name for :func:`halo_phases` (drop / merge / hoist)."""
+    return halo_phases(kernels, nranks)
+
+
+def dump_plan(kernels: Sequence, nranks: int, mode: Optional[str] = None,
+              updates: Sequence = ()) -> str:
+    """Listing 5/6/7-style text: the time loop with its
+    HaloSpots before lowering (``mode=None``) or the mode's update / wait
+    calls after lowering.  ``updates`` = solved equations printed (CSE'd,
+    aligned) inside the loop nest."""
+    an = halo_phases(kernels, nranks)
+    nd = None
+    lines = ["<Callable Kernel>"]
+    exprs = []
+    for eq in updates:
+        e = align_accesses(S.apply_cse(eq))
+        exprs += S.format_equation(e)
+    for k in kernels:
+        nd = len(k.radius)
+    if an.hoisted is not None:
+        names = ",".join(f.name for f, _t in an.hoisted.fields)
+        lines.append(f" <HaloSpot({names}) hoisted>" if mode is None
+                     else f" <HaloUpdateCall({names}) once>")
+    lines.append(" <[affine,sequential] Iteration time...>")
+    loops = ["x", "y", "z"][: nd or 3]
+
+    def nest(indent, region=""):
+        out = []
+        for i, ax in enumerate(loops):
+            tag = "[affine,parallel,vector-dim]" if i == len(loops) - 1 else "[affine,parallel]"
+            out.append(" " * (indent + i) + f"<{tag} Iteration {ax}{region}...>")
+        for e in exprs or ["<stencil update>"]:
+            out.append(" " * (indent + len(loops)) + f"<Expression {e}>")
+        return out
+
+    for ph in an.phases:
+        spot = ph.halo
+        names = ",".join(f.name for f, _t in spot.fields) if spot else ""
+        if spot is None:
+            lines += nest(2)
+        elif mode is None:
+            lines.append(f"  <HaloSpot({names})>")
+            lines += nest(2)
+        elif normalise_mode(mode) in ("basic", "diagonal"):
+            steps = len(loops) if normalise_mode(mode) == "basic" else 1
+            lines.append(f"  <HaloUpdateList({names}) steps={steps}>")
+            lines.append("   <HaloUpdateCall>")
+            lines.append(f"  <HaloWaitList({names})>")
+            lines += nest(2)
+        else:
+            lines.append(f"  <HaloUpdateList({names}) async>")
+            lines += nest(2, " CORE")
+            lines.append(f"  <HaloWaitList({names})>")
+            lines += nest(2, " REMAINDER")
+    return "\n".join(lines)
 
 
 def _fuse_pushes(acts, analysis: HaloAnalysis, decomp, rank: int) -> None:

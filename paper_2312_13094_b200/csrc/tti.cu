@@ -232,8 +232,8 @@ template <int R, class Op>
 static int launch_tti_stream(const Op& op, const Geom& g, const int64_t full[3],
                              const float* const* arrs, cudaStream_t st) {
   constexpr bool upd = Op::NF == 4;
-  if constexpr (R <= 3) return launch_stream_op<R, 16, 2>(op, g, full, arrs, st);
-  else if constexpr (R == 4) return launch_stream_op<R, upd ? 12 : 16, 2>(op, g, full, arrs, st);
+  if constexpr (R <= 2) return launch_stream_op<R, 16, 2>(op, g, full, arrs, st);
+  else if constexpr (R <= 4) return launch_stream_op<R, upd ? 12 : 16, 2>(op, g, full, arrs, st);
   else if constexpr (!upd || R == 5) return launch_stream_op<R, 8, 2>(op, g, full, arrs, st);
   else return launch_stream_op<R, 8, 1>(op, g, full, arrs, st);
 }

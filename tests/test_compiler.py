@@ -145,3 +145,33 @@ def test_c_abi_library_exports_every_declared_symbol():
     # error path without touching a GPU
     assert lib.sdmp_plan_add_action(None, None, 0, None, 0) == -1
     assert b"null" in lib.sdmp_last_error()
+
+
+def _format_access(eq):
+    return S.format_equation(eq)
+
+
+def test_align_accesses_spec_examples():
+    g = S.GridSpec((8, 8), (7.0, 7.0))
+    u = S.FieldSpec("u", g, 2, 1)
+    eq = S.StencilEquation(u.forward, u.at() + u.at(offsets=(-1, 0)))
+    al = CP.align_accesses(eq, (2, 2))
+    accs = sorted((a.tshift, a.offsets) for a in S.accesses(al.rhs))
+    assert accs == [(0, (1, 2)), (0, (2, 2))]           # u[t,x-1,y] -> u[t,x+1,y+2]
+    assert al.lhs.offsets == (2, 2)                       # u[t,x,y] -> u[t,x+2,y+2]
+    ident = CP.align_accesses(eq, (0, 0))
+    assert S.format_equation(ident) == S.format_equation(eq)
+    # default: each field's own halo (SO-2 -> 1)
+    assert CP.align_accesses(eq).lhs.offsets == tuple(u.halo)
+
+
+def test_dump_plan_listings():
+    eq, u, m = acoustic_eq(8, 3, 32)
+    k = CP.recognise([eq])[0]
+    pre = CP.dump_plan([k], 4, None, [eq])
+    assert "<HaloSpot(u)>" in pre and "Iteration time" in pre
+    basic = CP.dump_plan([k], 4, "basic", [eq])
+    assert "HaloUpdateCall" in basic and "HaloWaitList" in basic
+    full = CP.dump_plan([k], 4, "full", [eq])
+    assert full.index("CORE") < full.index("HaloWaitList") < full.index("REMAINDER")
+    assert "HaloSpot" not in CP.dump_plan([k], 1, None, [eq])
