@@ -71,6 +71,10 @@ class ClockSampler:
         self.path = f"/tmp/sdmp_clocks_{os.getpid()}.csv"
 
     def start(self):
+        """Start sampling and wait (<= 3 s) for the first sample, so the
+        timed region that follows is covered (the sample taken just before
+        it is kept as well: short regions still carry a reading)."""
+        self.n0 = 0
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
@@ -78,6 +82,17 @@ class ClockSampler:
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        t0 = time.time()
+        while time.time() - t0 < 3.0:
+            try:
+                n = sum(1 for _ in open(self.path))
+            except OSError:
+                n = 0
+            if n:
+                self.n0 = n - 1
+                return
+            time.sleep(0.01)
 
     def stop(self):
         if self.proc is None:
@@ -90,7 +105,7 @@ class ClockSampler:
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         try:
-            for line in open(self.path):
+            for line in list(open(self.path))[self.n0:]:
                 parts = [p.strip() for p in line.split(",")]
                 if len(parts) < 9:
                     continue

@@ -133,7 +133,7 @@ __device__ __forceinline__ void visco_point(const A& a, const ElCoef& k, typenam
   const T div = vadd(vadd(e[0], e[1]), e[2]);
   const T m2 = vcmul(2.f, M);  // exact
   const T base = vmul(vsub(L, m2), div);
-  const T ndti = vneg(vcmul(k.dt, I));
+  const T ndti = vcmul(-k.dt, I);  // = -RN(dt I) exactly
   visco_comp<0>(a, k, e, base, m2, M, ndti, s1, r1);
   visco_comp<1>(a, k, e, base, m2, M, ndti, s1, r1);
   visco_comp<2>(a, k, e, base, m2, M, ndti, s1, r1);

@@ -25,6 +25,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "tma.cuh"
 #include "vmath.cuh"
@@ -57,6 +58,19 @@ struct TMaps {
   CUtensorMap m[kMaxMaps];
 };
 
+// Op::kRing (optional, default false): unroll the x loop into a register ring
+template <class Op, class = void>
+struct RingOf {
+  static constexpr bool value = false;
+};
+template <class Op>
+struct RingOf<Op, std::void_t<decltype(Op::kRing)>> {
+#ifndef SDMP_RING
+#define SDMP_RING 1
+#endif
+  static constexpr bool value = SDMP_RING && Op::kRing;
+};
+
 template <int V> struct VType;
 template <> struct VType<1> { using T = float; };
 template <> struct VType<2> { using T = V2; };
@@ -77,10 +91,14 @@ template <int R, int TY, int V, int NF, int NC, int NP>
 struct StreamCtx {
   using L = SLayout<R, TY, V, NF, NC, NP>;
   using T = typename VType<V>::T;
-  const T (*w)[2 * R + 1];   // x-windows
+  static constexpr int W = 2 * R + 1;
+  const T (*w)[W];   // x-windows (register ring)
   const unsigned char* stage;
   int warp, lane;
-  __device__ __forceinline__ T xt(int f, int k) const { return w[f][R + k]; }
+  int rot;           // ring rotation = iteration % W (a constant after unrolling)
+  // plane x + k of front field f: loaded at iteration i - R + k, ring slot
+  // (i - R + k) mod W = (rot + R + 1 + k) mod W
+  __device__ __forceinline__ T xt(int f, int k) const { return w[f][(rot + R + 1 + k) % W]; }
   __device__ __forceinline__ const float* crow(int c, int dy) const {
     const float* base = reinterpret_cast<const float*>(stage + NF * L::FRONT + c * L::CENTER);
     return base + (warp + R + dy) * L::CZ + L::OFF + V * lane;
@@ -89,10 +107,17 @@ struct StreamCtx {
   __device__ __forceinline__ T ct(int c, int dy, int dz) const {
     const float* p = crow(c, dy) + dz;
     if constexpr (V == 2) {
-      if (dz & 1) {  // odd shift of a packed pair: from the two aligned pairs
+#ifndef SDMP_ODD_PAIR
+#define SDMP_ODD_PAIR 1  // measured faster than two 32-bit loads (r02 A/B)
+#endif
+#if SDMP_ODD_PAIR
+      if (dz & 1) {
         const V2 lo = vload<2>(p - 1), hi = vload<2>(p + 1);
         return v2pack(v2hi(lo), v2lo(hi));
       }
+#else
+      if (dz & 1) return v2pack(p[0], p[1]);  // odd shift: two 32-bit loads
+#endif
     }
     return vload<V>(p);
   }
@@ -178,30 +203,61 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
   const bool m0 = yin && z >= g.lo[2] && z < g.hi[2];
   const bool m1 = V > 1 && yin && z + 1 >= g.lo[2] && z + 1 < g.hi[2];
   const bool active = m0 || m1;
-  T w[NF > 0 ? NF : 1][2 * R + 1];
+  constexpr int W = 2 * R + 1;
+  T w[NF > 0 ? NF : 1][W];
 #pragma unroll
   for (int f = 0; f < NF; ++f)
 #pragma unroll
-    for (int k = 0; k <= 2 * R; ++k) w[f][k] = vconst<T>(0.f);
+    for (int k = 0; k < W; ++k) w[f][k] = vconst<T>(0.f);
 
-  for (int i = 0; i < nit; ++i) {
-    const int s = i % L::S;
-    mbar_wait(&full_bar[s], (i / L::S) & 1);
-    const unsigned char* st = sm + s * L::STAGE;
+  if constexpr (RingOf<Op>::value) {
+    // x-window as a register ring: the loop is unrolled by the window length
+    // W so every slot index is a compile-time constant (no register moves
+    // to slide the window; W x the code).  r02 A/B: no current op gains
+    // (TTI flat, visco velocity -12%), so none sets kRing.
+    for (int i0 = 0; i0 < nit; i0 += W) {
 #pragma unroll
-    for (int f = 0; f < NF; ++f) {
+      for (int j = 0; j < W; ++j) {
+        const int i = i0 + j;
+        if (i < nit) {
+          const int s = i % L::S;
+          mbar_wait(&full_bar[s], (i / L::S) & 1);
+          const unsigned char* st = sm + s * L::STAGE;
 #pragma unroll
-      for (int k = 0; k < 2 * R; ++k) w[f][k] = w[f][k + 1];
-      w[f][2 * R] = vload<V>(reinterpret_cast<const float*>(st + f * L::FRONT) +
-                             warp * L::TZ + V * lane);
+          for (int f = 0; f < NF; ++f)
+            w[f][j] = vload<V>(reinterpret_cast<const float*>(st + f * L::FRONT) + warp * L::TZ +
+                               V * lane);
+          if (i >= 2 * R && active) {
+            const int x = xa + i - 2 * R;
+            StreamCtx<R, TY, V, NF, NC, NP> ctx{w, st, warp, lane, j};
+            op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0, m1);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar[s]);
+        }
+      }
     }
-    if (i >= 2 * R && active) {
-      const int x = xa + i - 2 * R;
-      StreamCtx<R, TY, V, NF, NC, NP> ctx{w, st, warp, lane};
-      op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0, m1);
+  } else {
+    // sliding window: newest plane at slot 2R (rotation W - 1)
+    for (int i = 0; i < nit; ++i) {
+      const int s = i % L::S;
+      mbar_wait(&full_bar[s], (i / L::S) & 1);
+      const unsigned char* st = sm + s * L::STAGE;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+#pragma unroll
+        for (int k = 0; k < 2 * R; ++k) w[f][k] = w[f][k + 1];
+        w[f][2 * R] = vload<V>(reinterpret_cast<const float*>(st + f * L::FRONT) +
+                               warp * L::TZ + V * lane);
+      }
+      if (i >= 2 * R && active) {
+        const int x = xa + i - 2 * R;
+        StreamCtx<R, TY, V, NF, NC, NP> ctx{w, st, warp, lane, W - 1};
+        op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0, m1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[s]);
   }
 }
 

@@ -51,15 +51,15 @@ __device__ __forceinline__ typename A::T dcentral(const A& a, const float* w) {
 }
 
 // D_AX (a_AX g) with a, g both tapped: term_k = a(k) g(k) - a(-k) g(-k)
-// evaluated as fma(a(k), g(k), -(a(-k) g(-k))).
+// evaluated as fma(a(k), g(k), 0 - RN(a(-k) g(-k))).
 template <int R, int AX, int FA, int FG, class A>
 __device__ __forceinline__ typename A::T outer(const A& a, const float* w) {
   using T = typename A::T;
   T acc = vconst<T>(0.f);
 #pragma unroll
   for (int k = 1; k <= R; ++k) {
-    const T lo = vmul(a.template t<FA, AX>(-k), a.template t<FG, AX>(-k));
-    const T term = vfma(a.template t<FA, AX>(k), a.template t<FG, AX>(k), vneg(lo));
+    const T nlo = vnmul(a.template t<FA, AX>(-k), a.template t<FG, AX>(-k));
+    const T term = vfma(a.template t<FA, AX>(k), a.template t<FG, AX>(k), nlo);
     acc = vcfma(w[k], term, acc);
   }
   return acc;
@@ -105,9 +105,9 @@ __device__ __forceinline__ void u_point(const A& a, const TTICoef& c, typename A
   const T pp = vfma(d, gzr, vmul(e, h0));
   const T rr = vfma(d, h0, gzr);
   const T two = vconst<T>(2.f);
-  const T pt = vfma(two, c0, vneg(a.template q<QP2>()));   // 2 c0 exact
+  const T pt = vfma(two, c0, vnegz(a.template q<QP2>()));   // 2 c0 exact
   const T r0v = a.template q<QR0>();
-  const T rt = vfma(two, r0v, vneg(a.template q<QR2>()));
+  const T rt = vfma(two, r0v, vnegz(a.template q<QR2>()));
   p1 = vfma(sc, pp, pt);
   r1 = vfma(sc, rr, rt);
 }

@@ -44,6 +44,11 @@ __device__ __forceinline__ float vsub(float a, float b) { return __fsub_rn(a, b)
 __device__ __forceinline__ float vmul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float vfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ float vneg(float a) { return -a; }
+// 0 - a (exact negation up to the sign of zero): one FADD2 / folded into a
+// packed operand's negate modifier, where vneg costs two LOP3 per pair
+__device__ __forceinline__ float vnegz(float a) { return __fsub_rn(0.f, a); }
+// -(a b) rounded once, as 0 - RN(a b): ptxas emits FFMA2 -a, b, 0 for pairs
+__device__ __forceinline__ float vnmul(float a, float b) { return __fsub_rn(0.f, __fmul_rn(a, b)); }
 __device__ __forceinline__ float vdiv(float a, float b) { return __fdiv_rn(a, b); }
 // coefficient (uniform scalar) times value
 __device__ __forceinline__ float vcmul(float c, float b) { return __fmul_rn(c, b); }
@@ -72,6 +77,8 @@ __device__ __forceinline__ V2 vfma(V2 a, V2 b, V2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(o.r) : "l"(a.r), "l"(b.r), "l"(c.r));
   return o;
 }
+__device__ __forceinline__ V2 vnegz(V2 a) { return vsub(v2bcast(0.f), a); }
+__device__ __forceinline__ V2 vnmul(V2 a, V2 b) { return vsub(v2bcast(0.f), vmul(a, b)); }
 __device__ __forceinline__ V2 vneg(V2 a) {
   // sign flip of both lanes (exact)
   V2 o;

@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsdmp.so")
+LIB_PATH = os.environ.get("SDMP_LIB") or os.path.join(HERE, "libsdmp.so")  # SDMP_LIB: A/B builds
 
 SDMP_MAX_RADIUS = 8
 SDMP_NCOEF = SDMP_MAX_RADIUS + 1
