@@ -294,6 +294,7 @@ def main():
     launches = int(sum(r[5] for r in rows)) * args.steps
 
     pts_total = float(np.prod(shape))
+    arr_gb = 4.0 * math.prod(grid.local_shape) / 1e9
     value = pts_total * args.steps / (ms_max * 1e-3) / 1e9
 
     # dominant kernel: the largest compute action (CORE in full, DOMAIN else)
@@ -354,7 +355,7 @@ def main():
         torch.cuda.synchronize()
         ms_c = ctx.allreduce_max(e0.elapsed_time(e1))
         posts = [(i, a) for i, a in enumerate(ep.actions) if a.kind == "post" and a.messages]
-        sent = sum(m.volume for _i, a in posts for m in a.messages) * 4
+        sent = sum(m.volume * len(a.spot.fields) for _i, a in posts for m in a.messages) * 4
         post_ms = sum(rows[plan.native_index[i]][4] for i, _a in posts)
         fused = any(a.pushed for _i, a in posts)
         if fused:
@@ -373,6 +374,9 @@ def main():
                    "link_gbs_rank0": sent / (post_ms * 1e-3) / 1e9 if post_ms > 0 else None,
                    "link_peak_gbs": 900.0}
 
+    # per-rank action timings (skew between ranks shows up as WAIT time)
+    rank_actions = ctx.allgather([[int(r[2]), round(r[4], 4)] for r in rows]) if N > 1 else None
+
     cpu = None
     if ctx.rank == 0 and N == 1 and not args.no_cpu_baseline:
         try:
@@ -384,7 +388,8 @@ def main():
         line = {
             "metric": "GPts/s", "value": value, "unit": "GPts/s", "n_gpus": N,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "higher_is_better": True,
+            "scaling": "strong" if args.shape and N > 1 else "weak", "vs_baseline": None, "dtype": "fp32",
             "data": "synthetic (layered vp + hashed noise, Ricker source, receiver line)",
             "config": {"workload": (f"3D isotropic acoustic SO-{args.so}, {n}^3 per GPU "
                                     "(BASELINE configs[1])") if kname == "acoustic" and not args.shape
@@ -392,7 +397,7 @@ def main():
                        "global_shape": list(shape), "topology": list(topo), "mode": mode,
                        "parallelism": f"domain decomposition x/y {topo}",
                        "sources": 1, "receivers": args.nrec,
-                       "l2": "no flush: every array (4.5 GB) >> 126 MB L2"},
+                       "l2": f"no flush: every array ({arr_gb:.1f} GB per rank) >> 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": kernel_label,
@@ -405,6 +410,7 @@ def main():
             "cpu_baseline": cpu,
             "step_actions": [{"kind": int(r[2]), "stream": int(r[1]),
                               "ms": round(r[4], 4)} for r in rows],
+            "rank_actions": rank_actions,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -236,6 +236,7 @@ struct VelOp {
     vel_point<R>(a, k, o);
 #pragma unroll
     for (int q = 0; q < 3; ++q) vstore(out[q], idx, o[q], m0, m1);
+    c.push_out(o, 3, m0, m1);
   }
 };
 
@@ -269,6 +270,7 @@ struct StressOp {
     stress_point<R>(a, k, o);
 #pragma unroll
     for (int q = 0; q < 6; ++q) vstore(out[q], idx, o[q], m0, m1);
+    c.push_out(o, 6, m0, m1);
   }
 };
 
@@ -286,20 +288,27 @@ struct ViscoOp {
       vstore(out[q], idx, s1[q], m0, m1);
       vstore(out[6 + q], idx, r1[q], m0, m1);
     }
+    c.push_out(s1, 6, m0, m1);  // memory variables stay local
   }
 };
 
 // stream launch shape per radius: 2 z points per thread (packed fp32x2)
-// with 16 rows up to R = 4, 8 rows beyond (register budget)
+// with 16 rows up to R = 4, 8 rows beyond (register budget); 4-row tiles
+// for thin y-slabs (full-mode OWNED boxes R rows high)
 template <int R, class Op>
 static int launch_el_stream(const Op& op, const Geom& g, const int64_t full[3],
-                            const float* const* arrs, cudaStream_t st) {
+                            const float* const* arrs, cudaStream_t st, const Push& push) {
   // velocity (few operands, many taps) is issue bound: packed pairs; the
   // stress phases (8-15 pointwise operands) are bandwidth bound: one point
   // per thread keeps stages small and the ring deep (measured, r01).
   constexpr int V = Op::NP <= 4 ? 2 : 1;
-  if constexpr (R <= 4) return launch_stream_op<R, 16, V>(op, g, full, arrs, st);
-  else return launch_stream_op<R, 8, V>(op, g, full, arrs, st);
+  const int ny = g.hi[1] - g.lo[1];
+  if constexpr (R <= 4) {
+    if (ny <= 4) return launch_stream_op<R, 4, V>(op, g, full, arrs, st, &push);
+    return launch_stream_op<R, 16, V>(op, g, full, arrs, st, &push);
+  } else {
+    return launch_stream_op<R, 8, V>(op, g, full, arrs, st, &push);
+  }
 }
 
 // ---- host ----------------------------------------------------------------
@@ -326,12 +335,6 @@ static int launch_generic(const Geom& g, K kernel, const ElGeneric& params, cuda
   kernel<<<grid, b, 0, st>>>(params, push);
   SDMP_LAUNCHED();
   return SDMP_OK;
-}
-
-// Streaming pays off on thick boxes; thin OWNED slabs take the generic path.
-static bool stream_worth(const Geom& g, int radius) {
-  const int nx = g.hi[0] - g.lo[0], ny = g.hi[1] - g.lo[1];
-  return nx >= 4 * radius && ny >= 16;
 }
 
 static int variant_env() {
@@ -372,13 +375,11 @@ int elastic_velocity_impl(void* stream, const float* const v0[3],
   cudaStream_t st = (cudaStream_t)stream;
   const float* arrs[12] = {tau[0], tau[3], tau[4], tau[1], tau[2], tau[3], tau[4], tau[5],
                            v0[0], v0[1], v0[2], b};
-  if (variant_env() != 1 && push.ndir == 0 && stream_worth(p.g, radius) &&
-      stream_fits(p.g, radius) &&
-      tma_ok(full, arrs, 12)) {
+  if (variant_env() != 1 && stream_fits(p.g, radius) && tma_ok(full, arrs, 12)) {
     VelOp op{};
     for (int c = 0; c < 3; ++c) op.out[c] = v1[c];
     op.k = p.k;
-    RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st))
+    RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st, push))
   }
   RADIUS_SWITCH(launch_generic(p.g, el_velocity<RR>, p, st, push))
 }
@@ -402,13 +403,11 @@ int elastic_stress_impl(void* stream, const float* const v1[3],
   cudaStream_t st = (cudaStream_t)stream;
   const float* arrs[14] = {v1[0], v1[1], v1[2], v1[0], v1[1], v1[2],
                            t0[0], t0[1], t0[2], t0[3], t0[4], t0[5], lam, mu};
-  if (variant_env() != 1 && push.ndir == 0 && stream_worth(p.g, radius) &&
-      stream_fits(p.g, radius) &&
-      tma_ok(full, arrs, 14)) {
+  if (variant_env() != 1 && stream_fits(p.g, radius) && tma_ok(full, arrs, 14)) {
     StressOp op{};
     for (int c = 0; c < 6; ++c) op.out[c] = t1[c];
     op.k = p.k;
-    RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st))
+    RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st, push))
   }
   RADIUS_SWITCH(launch_generic(p.g, el_stress<RR>, p, st, push))
 }
@@ -439,13 +438,11 @@ int visco_stress_impl(void* stream, const float* const v1[3],
   const float* arrs[21] = {v1[0], v1[1], v1[2], v1[0], v1[1], v1[2],
                            s0[0], s0[1], s0[2], s0[3], s0[4], s0[5],
                            r0[0], r0[1], r0[2], r0[3], r0[4], r0[5], prm[0], prm[1], prm[2]};
-  if (variant_env() != 1 && push.ndir == 0 && stream_worth(p.g, radius) &&
-      stream_fits(p.g, radius) &&
-      tma_ok(full, arrs, 21)) {
+  if (variant_env() != 1 && stream_fits(p.g, radius) && tma_ok(full, arrs, 21)) {
     ViscoOp op{};
     for (int c = 0; c < 12; ++c) op.out[c] = p.out[c];
     op.k = p.k;
-    RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st))
+    RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st, push))
   }
   RADIUS_SWITCH(launch_generic(p.g, visco_stress<RR>, p, st, push))
 }

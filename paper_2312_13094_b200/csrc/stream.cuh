@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "common.cuh"
 #include "tma.cuh"
 #include "vmath.cuh"
 
@@ -96,6 +97,8 @@ struct StreamCtx {
   const unsigned char* stage;
   int warp, lane;
   int rot;           // ring rotation = iteration % W (a constant after unrolling)
+  const Push* push;  // fused halo push (full mode OWNED slabs), ndir 0 = none
+  int x, y, z;       // FULL coordinates of the thread's first point
   // plane x + k of front field f: loaded at iteration i - R + k, ring slot
   // (i - R + k) mod W = (rot + R + 1 + k) mod W
   __device__ __forceinline__ T xt(int f, int k) const { return w[f][(rot + R + 1 + k) % W]; }
@@ -121,12 +124,44 @@ struct StreamCtx {
     }
     return vload<V>(p);
   }
+  // store n outputs of this thread's points into every neighbour HALO whose
+  // receive box contains them (peer pointers over NVLink)
+  __device__ __forceinline__ void push_out(const T* v, int n, bool m0, bool m1) const {
+    if (push->ndir) push_vals(*push, x, y, z, v, n, m0, m1);
+  }
   __device__ __forceinline__ T pt(int q) const {
     const float* base = reinterpret_cast<const float*>(stage + NF * L::FRONT + NC * L::CENTER +
                                                        q * L::FRONT);
     return vload<V>(base + warp * L::TZ + V * lane);
   }
 };
+
+// fused push of one thread's points (float: one point; V2: z, z + 1)
+__device__ __forceinline__ void push_vals(const Push& P, int x, int y, int z, const float* v,
+                                          int n, bool m0, bool) {
+  if (m0) push_point(P, x, y, z, v, n);
+}
+__device__ __forceinline__ void push_vals(const Push& P, int x, int y, int z, const V2* v, int n,
+                                          bool m0, bool m1) {
+  for (int d = 0; d < P.ndir; ++d) {
+    const PushGeo& g = P.geo[d];
+    if (x < g.lo[0] || x >= g.hi[0] || y < g.lo[1] || y >= g.hi[1]) continue;
+    const bool in0 = m0 && z >= g.lo[2] && z < g.hi[2];
+    const bool in1 = m1 && z + 1 >= g.lo[2] && z + 1 < g.hi[2];
+    if (!in0 && !in1) continue;
+    const int64_t j = (int64_t)(x + g.off[0]) * g.psx + (int64_t)(y + g.off[1]) * g.psy +
+                      (z + g.off[2]);
+    for (int q = 0; q < n && q < P.nout; ++q) {
+      float* dst = P.base[q][d] + j;
+      if (in0 && in1 && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+        *reinterpret_cast<uint64_t*>(dst) = v[q].r;
+      } else {
+        if (in0) dst[0] = v2lo(v[q]);
+        if (in1) dst[1] = v2hi(v[q]);
+      }
+    }
+  }
+}
 
 // masked store of V consecutive values at idx (m0: first point, m1: second)
 __device__ __forceinline__ void vstore(float* p, int64_t idx, float v, bool m0, bool) {
@@ -143,7 +178,8 @@ __device__ __forceinline__ void vstore(float* p, int64_t idx, V2 v, bool m0, boo
 
 template <int R, int TY, int V, class Op>
 __global__ void __launch_bounds__(SLayout<R, TY, V, Op::NF, Op::NC, Op::NP>::THREADS, 1)
-stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, const int xchunk) {
+stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, const int xchunk,
+              const __grid_constant__ Push push) {
   constexpr int NF = Op::NF, NC = Op::NC, NP = Op::NP;
   using L = SLayout<R, TY, V, NF, NC, NP>;
   using T = typename VType<V>::T;
@@ -229,7 +265,7 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
                                V * lane);
           if (i >= 2 * R && active) {
             const int x = xa + i - 2 * R;
-            StreamCtx<R, TY, V, NF, NC, NP> ctx{w, st, warp, lane, j};
+            StreamCtx<R, TY, V, NF, NC, NP> ctx{w, st, warp, lane, j, &push, x, y, z};
             op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0, m1);
           }
           __syncwarp();
@@ -252,7 +288,7 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
       }
       if (i >= 2 * R && active) {
         const int x = xa + i - 2 * R;
-        StreamCtx<R, TY, V, NF, NC, NP> ctx{w, st, warp, lane, W - 1};
+        StreamCtx<R, TY, V, NF, NC, NP> ctx{w, st, warp, lane, W - 1, &push, x, y, z};
         op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0, m1);
       }
       __syncwarp();
@@ -283,7 +319,7 @@ inline int stream_chunks(int64_t tiles, int nx, int R) {
 // point arrays (all FULL-shaped, same `full`).
 template <int R, int TY, int V, class Op>
 int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const float* const* ptrs,
-                     cudaStream_t st) {
+                     cudaStream_t st, const Push* push = nullptr) {
   using L = SLayout<R, TY, V, Op::NF, Op::NC, Op::NP>;
   static_assert(Op::NF + Op::NC + Op::NP <= kMaxMaps, "too many tensor maps");
   static int attr_dev = -1;
@@ -323,7 +359,9 @@ int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const f
             R, TY, V, Op::NF, Op::NC, Op::NP, g.lo[0], g.lo[1], g.lo[2], g.hi[0], g.hi[1],
             g.hi[2], (long)full[0], (long)full[1], (long)full[2], tz, ty, nch, chunk, L::BYTES,
             L::S, L::STAGE);
-  stream_kernel<R, TY, V, Op><<<grid, block, L::BYTES, st>>>(maps, op, g, chunk);
+  const Push nopush{};
+  stream_kernel<R, TY, V, Op><<<grid, block, L::BYTES, st>>>(maps, op, g, chunk,
+                                                             push ? *push : nopush);
   SDMP_LAUNCHED();
   if (dbg) {
     cudaError_t e = cudaStreamSynchronize(st);

@@ -222,6 +222,8 @@ struct UOp {
     u_point<R>(a, k, p1, r1);
     vstore(out[0], idx, p1, m0, m1);
     vstore(out[1], idx, r1, m0, m1);
+    const typename Ctx::T o[2] = {p1, r1};
+    c.push_out(o, 2, m0, m1);
   }
 };
 
@@ -230,12 +232,22 @@ struct UOp {
 // fewer rows as R grows; scalar for the widest update stencils.
 template <int R, class Op>
 static int launch_tti_stream(const Op& op, const Geom& g, const int64_t full[3],
-                             const float* const* arrs, cudaStream_t st) {
+                             const float* const* arrs, cudaStream_t st,
+                             const Push* push = nullptr) {
   constexpr bool upd = Op::NF == 4;
-  if constexpr (R <= 2) return launch_stream_op<R, 16, 2>(op, g, full, arrs, st);
-  else if constexpr (R <= 4) return launch_stream_op<R, upd ? 12 : 16, 2>(op, g, full, arrs, st);
-  else if constexpr (!upd || R == 5) return launch_stream_op<R, 8, 2>(op, g, full, arrs, st);
-  else return launch_stream_op<R, 8, 1>(op, g, full, arrs, st);
+  // thin y-slabs (full-mode OWNED boxes, SO rows high): matching tile height
+  const int ny = g.hi[1] - g.lo[1];
+  if constexpr (R <= 2) {
+    if (ny <= 4) return launch_stream_op<R, 4, 2>(op, g, full, arrs, st, push);
+    return launch_stream_op<R, 16, 2>(op, g, full, arrs, st, push);
+  } else if constexpr (R <= 4) {
+    if (ny <= 8) return launch_stream_op<R, 8, 2>(op, g, full, arrs, st, push);
+    return launch_stream_op<R, upd ? 12 : 16, 2>(op, g, full, arrs, st, push);
+  } else if constexpr (!upd || R == 5) {
+    return launch_stream_op<R, 8, 2>(op, g, full, arrs, st, push);
+  } else {
+    return launch_stream_op<R, 8, 1>(op, g, full, arrs, st, push);
+  }
 }
 
 // FULL-shaped scratch pair per (device, size), grow-only, never freed
@@ -282,9 +294,7 @@ static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const P
   const float* a2[15] = {p.tap[TAX], p.tap[TGP], p.tap[TGR], p.tap[TP],
                          p.tap[TAY], p.tap[TAZ], p.tap[TGP], p.tap[TGR], p.tap[TP],
                          p.pnt[QP2], p.pnt[QR0], p.pnt[QR2], p.pnt[QM], p.pnt[QE], p.pnt[QD]};
-  const bool thick = (p.g.hi[0] - p.g.lo[0]) >= 4 * R && (p.g.hi[1] - p.g.lo[1]) >= 16;
-  const bool stream = variant_env() != 1 && push.ndir == 0 && thick && stream_fits(p1.g, R) &&
-                      stream_fits(p.g, R) &&
+  const bool stream = variant_env() != 1 && stream_fits(p1.g, R) && stream_fits(p.g, R) &&
                       tma_ok(full, a1, 7) && tma_ok(full, a2, 15);
   dim3 b(32, 8);
   if (stream) {
@@ -298,7 +308,7 @@ static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const P
     u.out[0] = p.out[0];
     u.out[1] = p.out[1];
     u.k = p.c;
-    return launch_tti_stream<R>(u, p.g, full, a2, st);
+    return launch_tti_stream<R>(u, p.g, full, a2, st, &push);
   }
   dim3 g1((p1.g.hi[2] - p1.g.lo[2] + 31) / 32, (p1.g.hi[1] - p1.g.lo[1] + 7) / 8,
           p1.g.hi[0] - p1.g.lo[0]);

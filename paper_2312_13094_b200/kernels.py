@@ -53,25 +53,50 @@ def hash_uniform(gx, gy, gz, seed: int = 0):
     return (h & 0xFFFFFF) / float(1 << 24)
 
 
-def _global_index_grids(fn: Function, torch):
-    ext = fn.grid.local_extent
-    dev = fn.storage.device
-    idx = [torch.arange(a, b, device=dev, dtype=torch.int64) for a, b in ext]
-    while len(idx) < 3:
-        idx.append(torch.zeros(1, device=dev, dtype=torch.int64))
-    return torch.meshgrid(*idx, indexing="ij")
-
-
-def layered_vp(fn: Function, vmin=1.5, vmax=4.5, noise=0.01, seed=0):
+def _vp_law(gx, gy, gz, nz, vmin=1.5, vmax=4.5, noise=0.01, seed=0):
     """vp(z) = vmin + (vmax - vmin) k/(nz-1), times (1 + noise U(-1,1))
-    (SURVEY.md §8d C1 law), evaluated on this rank's DOMAIN in fp64, as a
-    torch tensor on the device (same shape as the DOMAIN view)."""
-    import torch
-    gx, gy, gz = _global_index_grids(fn, torch)
-    nz = fn.grid.shape[-1]
+    (SURVEY.md §8d C1 law), fp64, from global index grids."""
     base = vmin + (vmax - vmin) * gz.double() / max(nz - 1, 1)
     u = hash_uniform(gx, gy, gz, seed).double()
     return base * (1.0 + noise * (2.0 * u - 1.0))
+
+
+def _fill(fns: Sequence[Function], f, max_points: int = 1 << 25):
+    """Write ``f(gx, gy, gz)`` (a tuple of fp64 tensors, one per field) into
+    the DOMAIN of each static field, slab by slab along x so the fp64 /
+    int64 temporaries stay bounded (a 1536^3 TTI rank would otherwise need
+    tens of GB of index grids)."""
+    import torch
+    ref = fns[0]
+    ext = list(ref.grid.local_extent)
+    dev = ref.storage.device
+    while len(ext) < 3:
+        ext.append((0, 1))
+    (xa, xb), (ya, yb), (za, zb) = ext
+    gy_ = torch.arange(ya, yb, device=dev, dtype=torch.int64)
+    gz_ = torch.arange(za, zb, device=dev, dtype=torch.int64)
+    chunk = max(1, max_points // max(1, (yb - ya) * (zb - za)))
+    views = [fn._domain_view(0) for fn in fns]
+    for x0 in range(xa, xb, chunk):
+        x1 = min(xb, x0 + chunk)
+        gx_ = torch.arange(x0, x1, device=dev, dtype=torch.int64)
+        gx, gy, gz = torch.meshgrid(gx_, gy_, gz_, indexing="ij")
+        vals = f(gx, gy, gz)
+        for v, val in zip(views, vals):
+            v[x0 - xa:x1 - xa].copy_(val.reshape(v[x0 - xa:x1 - xa].shape).to(v.dtype))
+
+
+def layered_vp(fn: Function, vmin=1.5, vmax=4.5, noise=0.01, seed=0):
+    """:func:`_vp_law` on this rank's DOMAIN (device tensor, DOMAIN shape;
+    small grids only, the models fill slab by slab)."""
+    import torch
+    ext = list(fn.grid.local_extent)
+    while len(ext) < 3:
+        ext.append((0, 1))
+    dev = fn.storage.device
+    gx, gy, gz = torch.meshgrid(*[torch.arange(a, b, device=dev, dtype=torch.int64)
+                                  for a, b in ext], indexing="ij")
+    return _vp_law(gx, gy, gz, fn.grid.shape[-1], vmin, vmax, noise, seed)
 
 
 def layered_vp_numpy(shape, vmin=1.5, vmax=4.5, noise=0.01, seed=0):
@@ -108,8 +133,11 @@ def acoustic_model(grid: Grid, so: int = 8, vp=None, name: str = "u") -> KernelD
     import torch
     u = TimeFunction(name=name, grid=grid, space_order=so, time_order=2)
     m = Function(name=f"m_{name}", grid=grid, space_order=so)
-    vals = layered_vp(m) if vp is None else vp
-    _set_domain(m, (1.0 / vals ** 2).float())
+    nz = grid.shape[-1]
+    if vp is None:
+        _fill([m], lambda gx, gy, gz: (1.0 / _vp_law(gx, gy, gz, nz) ** 2,))
+    else:
+        _set_domain(m, (1.0 / vp ** 2).float())
     eq = Eq(u.forward, solve(m * u.dt2 - u.laplace, u.forward))
     return KernelDef("acoustic", {"u": u, "m": m}, [], [eq], bytes_per_point=16, working_set=4)
 
@@ -138,19 +166,22 @@ def tti_model(grid: Grid, so: int = 8, vp=None) -> KernelDef:
     epsp = Function(name="epsp", grid=grid, space_order=so)
     delp = Function(name="delp", grid=grid, space_order=so)
     a = [Function(name=f"a{c}", grid=grid, space_order=so) for c in "xyz"]
-    vals = layered_vp(m) if vp is None else vp
-    _set_domain(m, (1.0 / vals ** 2).float())
-    gx, gy, gz = _global_index_grids(m, torch)
     nz = grid.shape[-1]
-    eps = 0.25 * gz.double() / max(nz - 1, 1)
-    dlt = 0.4 * eps
-    th = math.radians(30.0) + math.radians(5.0) * hash_uniform(gx, gy, gz, 11).double()
-    ph = math.radians(20.0) + math.radians(5.0) * hash_uniform(gx, gy, gz, 12).double()
-    _set_domain(epsp, (1.0 + 2.0 * eps).float())
-    _set_domain(delp, torch.sqrt(1.0 + 2.0 * dlt).float())
-    _set_domain(a[0], (torch.sin(th) * torch.cos(ph)).float())
-    _set_domain(a[1], (torch.sin(th) * torch.sin(ph)).float())
-    _set_domain(a[2], torch.cos(th).float())
+
+    def law(gx, gy, gz):
+        eps = 0.25 * gz.double() / max(nz - 1, 1)
+        dlt = 0.4 * eps
+        th = math.radians(30.0) + math.radians(5.0) * hash_uniform(gx, gy, gz, 11).double()
+        ph = math.radians(20.0) + math.radians(5.0) * hash_uniform(gx, gy, gz, 12).double()
+        out = (1.0 + 2.0 * eps, torch.sqrt(1.0 + 2.0 * dlt), torch.sin(th) * torch.cos(ph),
+               torch.sin(th) * torch.sin(ph), torch.cos(th))
+        if vp is None:
+            out = (1.0 / _vp_law(gx, gy, gz, nz) ** 2,) + out
+        return out
+
+    _fill(([m] if vp is None else []) + [epsp, delp] + a, law)
+    if vp is not None:
+        _set_domain(m, (1.0 / vp ** 2).float())
     k = CP.TTIKernel(p.spec, r.spec, m.spec, epsp.spec, delp.spec,
                      (a[0].spec, a[1].spec, a[2].spec), so)
     fields = {"p": p, "r": r, "m": m, "epsp": epsp, "delp": delp, "ax": a[0], "ay": a[1],
@@ -166,10 +197,10 @@ TNAMES = ("txx", "tyy", "tzz", "txy", "txz", "tyz")
 RNAMES = ("rxx", "ryy", "rzz", "rxy", "rxz", "ryz")
 
 
-def _elastic_materials(ref: Function):
+def _elastic_materials(gx, gy, gz, nz):
     """vp law as acoustic, vs = vp/sqrt(3), rho = 0.31 (1000 vp)^0.25 (g/cc,
     Gardner), lam = rho (vp^2 - 2 vs^2), mu = rho vs^2, b = 1/rho."""
-    vp = layered_vp(ref)
+    vp = _vp_law(gx, gy, gz, nz)
     vs = vp / math.sqrt(3.0)
     rho = 0.31 * (1000.0 * vp) ** 0.25
     return vp, vs, rho
@@ -183,10 +214,13 @@ def elastic_model(grid: Grid, so: int = 8) -> KernelDef:
     b = Function(name="b_el", grid=grid, space_order=so)
     lam = Function(name="lam", grid=grid, space_order=so)
     mu = Function(name="mu", grid=grid, space_order=so)
-    vp, vs, rho = _elastic_materials(b)
-    _set_domain(b, (1.0 / rho).float())
-    _set_domain(lam, (rho * (vp ** 2 - 2.0 * vs ** 2)).float())
-    _set_domain(mu, (rho * vs ** 2).float())
+    nz = grid.shape[-1]
+
+    def law(gx, gy, gz):
+        vp, vs, rho = _elastic_materials(gx, gy, gz, nz)
+        return 1.0 / rho, rho * (vp ** 2 - 2.0 * vs ** 2), rho * vs ** 2
+
+    _fill([b, lam, mu], law)
     kv = CP.StaggeredPhase("v", tuple(f.spec for f in v), tuple(f.spec for f in t),
                            (b.spec,), so=so)
     kt = CP.StaggeredPhase("t", tuple(f.spec for f in v), tuple(f.spec for f in t),
@@ -211,7 +245,6 @@ def viscoelastic_model(grid: Grid, so: int = 16, qp: float = 100.0, qs: float = 
     l2m = Function(name="l2m", grid=grid, space_order=so)
     mus = Function(name="mus", grid=grid, space_order=so)
     its = Function(name="its", grid=grid, space_order=so)
-    vp, vs, rho = _elastic_materials(b)
     w0 = 2.0 * math.pi * f0
 
     def taus(q):
@@ -222,12 +255,16 @@ def viscoelastic_model(grid: Grid, so: int = 16, qp: float = 100.0, qs: float = 
     ts_p, te_p = taus(qp)
     ts_s, te_s = taus(qs)
     t_sigma = ts_p  # one stress relaxation time for P and S (PAPER.md Table)
-    lam = rho * (vp ** 2 - 2.0 * vs ** 2)
-    mu_ = rho * vs ** 2
-    _set_domain(b, (1.0 / rho).float())
-    _set_domain(l2m, ((lam + 2.0 * mu_) * (te_p / t_sigma)).float())
-    _set_domain(mus, (mu_ * (te_s / t_sigma)).float())
-    _set_domain(its, (1.0 / t_sigma) * (rho * 0.0 + 1.0).float())
+    nz = grid.shape[-1]
+
+    def law(gx, gy, gz):
+        vp, vs, rho = _elastic_materials(gx, gy, gz, nz)
+        lam = rho * (vp ** 2 - 2.0 * vs ** 2)
+        mu_ = rho * vs ** 2
+        return (1.0 / rho, (lam + 2.0 * mu_) * (te_p / t_sigma), mu_ * (te_s / t_sigma),
+                rho * 0.0 + 1.0 / t_sigma)
+
+    _fill([b, l2m, mus, its], law)
     kv = CP.StaggeredPhase("v", tuple(f.spec for f in v), tuple(f.spec for f in s),
                            (b.spec,), so=so)
     kt = CP.StaggeredPhase("visco_t", tuple(f.spec for f in v), tuple(f.spec for f in s),

@@ -9,6 +9,7 @@ regions over NVLink (peer pointers imported with cudaIpcOpenMemHandle).
 from __future__ import annotations
 
 import math
+import os
 from fractions import Fraction
 from typing import Dict, List
 
@@ -166,7 +167,6 @@ class NativeOperatorPlan:
             self._encode_static(ep, decomp, rank)
         # CUDA-graph replay of whole buffer-rotation periods (SDMP_GRAPH=0
         # disables); removes per-step launch overhead on small grids
-        import os
         self.plan.set_graph(os.environ.get("SDMP_GRAPH", "1") != "0")
 
     # ------------------------------------------------------------------
@@ -231,7 +231,10 @@ class NativeOperatorPlan:
         return ints
 
     def _post_ints(self, a, fid, pfid, pflag, decomp, rank):
-        ints = [R.ACT["POST"], a.stream, a.phase, 0, 16 if a.pushed else 0]
+        # SDMP_COPY_ENGINE=sm: halo copies as SM kernels storing over NVLink
+        # (default: copy engines, cudaMemcpy3DAsync)
+        eng = 1 if os.environ.get("SDMP_COPY_ENGINE", "ce") == "sm" else 0
+        ints = [R.ACT["POST"], a.stream, a.phase, 0, (16 if a.pushed else 0) | eng]
         n = 0
         for m in a.messages:
             for f, t in a.spot.fields:
