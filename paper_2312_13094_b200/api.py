@@ -154,6 +154,7 @@ class Data:
                 fn.storage.device)
             if fn.grid.ndims == 2:
                 val = val.unsqueeze(-1)
+        fn._version += 1
         for b in self._buffers(tsel, True):
             view = fn._domain_view(b)
             sl = tuple(slice(l, h) for l, h in loc)
@@ -251,6 +252,9 @@ class Function:
         self.storage = torch.zeros((self.time_buffers,) + self.full3, dtype=torch.float32,
                                    device=dev)
         self._latest = 0
+        # bumped by every Data write: plans re-bind derived buffers (dt^2/m)
+        # and re-exchange static halos only when a static field changed
+        self._version = 0
 
     # -- storage helpers ---------------------------------------------------
     @property

@@ -84,6 +84,8 @@ def _fill(fns: Sequence[Function], f, max_points: int = 1 << 25):
         vals = f(gx, gy, gz)
         for v, val in zip(views, vals):
             v[x0 - xa:x1 - xa].copy_(val.reshape(v[x0 - xa:x1 - xa].shape).to(v.dtype))
+    for fn in fns:
+        fn._version += 1
 
 
 def layered_vp(fn: Function, vmin=1.5, vmax=4.5, noise=0.01, seed=0):
@@ -116,6 +118,7 @@ def _set_domain(fn: Function, values):
     """Write a DOMAIN-shaped device tensor into buffer 0 of a static field."""
     v = fn._domain_view(0)
     v.copy_(values.reshape(v.shape).to(v.dtype))
+    fn._version += 1
 
 
 def critical_dt(vmax: float, spacing: Sequence[float], courant: float = 0.38) -> float:

@@ -72,6 +72,7 @@ class NativeOperatorPlan:
         ep = self.eplan
         self.plan = R.NativePlan(ctx.device or 0, ep.phases_per_step, rank)
         self.static = None
+        self._seen = {}  # static-field versions the bound buffers reflect
         self.keep = []
         self.fid: Dict[S.FieldSpec, int] = {}
         for spec, fn in op.fields.items():
@@ -349,11 +350,18 @@ class NativeOperatorPlan:
                 entry[3].copy_(torch.from_numpy(np.ascontiguousarray(t.sparse.data, np.float32)))
             else:
                 entry[2].zero_()
+        # bound dt^2/m buffers and the hoisted exchange of static fields are
+        # redone only when a static field changed (Data writes bump _version)
         for sbuf, mfn, C in self.scale_bufs:
-            R.bind_scale(sbuf, mfn.storage[0], C)
+            if self._seen.get(id(sbuf)) != mfn._version:
+                R.bind_scale(sbuf, mfn.storage[0], C)
+                self._seen[id(sbuf)] = mfn._version
         if self.static is not None:
-            self.static.run(0, 0)
-            self.static.sync()
+            ver = tuple(self.op.fields[f]._version for f, _t in self.eplan.hoisted.fields)
+            if self._seen.get("static") != ver:
+                self.static.run(0, 0)
+                self.static.sync()
+                self._seen["static"] = ver
         self.plan.run(time_m, time_M)
         self.plan.sync()
 

@@ -209,3 +209,29 @@ def test_graph_replay_long_run(monkeypatch):
         res.append((u.data_gather(), rec.data.copy()))
     assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
     assert np.abs(res[1][1]).max() > 0
+
+
+def test_static_field_update_between_applies():
+    """dt^2/m is re-bound only when m changes (Data writes bump its version):
+    changing m between two applies must give the same result as an operator
+    built on the changed m from the start; an unchanged m is not re-bound."""
+    shape, so, steps = (24, 20, 28), 8, 8
+
+    def build(tag):
+        grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
+        kd = KD.acoustic_model(grid, so=so, name=f"u_{tag}")
+        u, m = kd.fields["u"], kd.fields["m"]
+        u.data[:, 10, 10, 14] = 1.0
+        return u, m, Operator([kd])
+
+    dt = float(np.float32(KD.critical_dt(4.6, (10.0,) * 3)))
+    u1, m1, op1 = build("sv1")
+    op1.apply(time_M=0, dt=dt)           # binds dt^2/m with the original m
+    m1.data[...] = m1.data[...] * np.float32(0.5)
+    u1.data[...] = 0.0
+    u1.data[:, 10, 10, 14] = 1.0
+    op1.apply(time_M=steps - 1, dt=dt)
+    u2, m2, op2 = build("sv2")
+    m2.data[...] = m2.data[...] * np.float32(0.5)
+    op2.apply(time_M=steps - 1, dt=dt)
+    assert np.array_equal(u1.data_gather(), u2.data_gather())
