@@ -20,8 +20,11 @@
 //    is staged in shared memory for the y/z taps.  u0 is read from DRAM once
 //    (halo re-reads of neighbouring tiles hit L2), u2 and m are streamed
 //    once (evict-first), u1 written once: 16 B / point.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tma.cuh"
+#include "vmath.cuh"
 
 namespace sdmp {
 
@@ -108,6 +111,10 @@ __device__ __forceinline__ float4 ld4(const float* p) {
 }
 __device__ __forceinline__ float4 ld4_stream(const float* p) {
   return __ldcs(reinterpret_cast<const float4*>(p));
+}
+// lanes (x, y) or (z, w) of a float4 as one packed pair
+__device__ __forceinline__ V2 f4pair(const float4& v, int h) {
+  return h == 0 ? v2pack(v.x, v.y) : v2pack(v.z, v.w);
 }
 __device__ __forceinline__ float f4get(const float4& v, int j) {
   return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
@@ -259,6 +266,14 @@ struct TmaCfg {
   static constexpr int THREADS = 32 * (TY + 1);
 };
 
+// x-window as an unrolled register ring (no per-plane register moves) for
+// the wide stencils; SDMP_STAR_RING_MIN sets the smallest radius using it
+#ifndef SDMP_STAR_RING_MIN
+#define SDMP_STAR_RING_MIN 1
+#endif
+template <int R>
+constexpr bool kStarRing = R >= SDMP_STAR_RING_MIN && R <= 4;  // r02 A/B: wide stencils lose
+
 template <int R, int TY>
 __global__ void __launch_bounds__(TmaCfg<R, TY>::THREADS, 1)
 star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ CUtensorMap tm_center,
@@ -317,18 +332,15 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
   const bool active = (z < p.g.hi[2]) && (y < p.g.hi[1]);
   const int64_t sx = p.g.sx, sy = p.g.sy;
   const int64_t col = (int64_t)y * sy + z;
-  float4 w[2 * R + 1];
+  constexpr int W = 2 * R + 1;
+  float4 w[W];
 #pragma unroll
-  for (int k = 0; k <= 2 * R; ++k) w[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k = 0; k < W; ++k) w[k] = make_float4(0.f, 0.f, 0.f, 0.f);
 
-  for (int i = 0; i < nit; ++i) {
-    const int s = i % T::S;
-    mbar_wait(&full_bar[s], (i / T::S) & 1);
-    const unsigned char* st = sm + s * T::STAGE;
-#pragma unroll
-    for (int k = 0; k < 2 * R; ++k) w[k] = w[k + 1];
-    w[2 * R] = *reinterpret_cast<const float4*>(
-        reinterpret_cast<const float*>(st) + warp * kTZ + 4 * lane);
+  // one pipeline iteration; the x-window plane of logical index kk (0 =
+  // oldest, 2R = newest) sits in register slot (rot + kk + 1) % W
+  auto consume = [&](int i, int rot, const unsigned char* st) {
+    auto wv = [&](int kk) -> const float4& { return w[(rot + kk + 1) % W]; };
     if (i >= 2 * R && active) {
       const int x = xa + i - 2 * R;
       const float* row = reinterpret_cast<const float*>(st + T::FRONT) + (warp + R) * T::CZ +
@@ -348,31 +360,64 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
         mv = *reinterpret_cast<const float4*>(
             reinterpret_cast<const float*>(st + 2 * T::FRONT + T::CENTER) + warp * kTZ + 4 * lane);
       // same operation order per point as star_point (x, y, z taps; k
-      // ascending), vectorised over the 4 z points of this thread
-      float lap[4], out[4];
+      // ascending), on the 4 z points of this thread as two packed fp32x2
+      // pairs (FFMA2 / FADD2: per-lane IEEE ops, identical bits).  Odd z
+      // shifts straddle the register pairs, so those taps run per lane.
+      V2 lap[2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) lap[j] = __fmul_rn(p.csum0, f4get(w[R], j));
+      for (int h = 0; h < 2; ++h) lap[h] = vcmul(p.csum0, f4pair(wv(R), h));
 #pragma unroll
       for (int k = 1; k <= R; ++k)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          lap[j] = __fmaf_rn(p.c[0][k], __fadd_rn(f4get(w[R - k], j), f4get(w[R + k], j)), lap[j]);
+        for (int h = 0; h < 2; ++h)
+          lap[h] = vcfma(p.c[0][k], vadd(f4pair(wv(R - k), h), f4pair(wv(R + k), h)), lap[h]);
 #pragma unroll
       for (int k = 1; k <= R; ++k) {
         const float4 a = *reinterpret_cast<const float4*>(row - k * T::CZ);
         const float4 b = *reinterpret_cast<const float4*>(row + k * T::CZ);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          lap[j] = __fmaf_rn(p.c[1][k], __fadd_rn(f4get(a, j), f4get(b, j)), lap[j]);
+        for (int h = 0; h < 2; ++h)
+          lap[h] = vcfma(p.c[1][k], vadd(f4pair(a, h), f4pair(b, h)), lap[h]);
       }
 #pragma unroll
-      for (int k = 1; k <= R; ++k)
+      for (int k = 1; k <= R; ++k) {
+        if ((k & 1) == 0) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          lap[j] = __fmaf_rn(p.c[2][k], __fadd_rn(zw[T::OFF + j - k], zw[T::OFF + j + k]), lap[j]);
+          for (int h = 0; h < 2; ++h) {
+            const int lo = T::OFF + 2 * h - k, hi = T::OFF + 2 * h + k;
+            lap[h] = vcfma(p.c[2][k], vadd(v2pack(zw[lo], zw[lo + 1]), v2pack(zw[hi], zw[hi + 1])),
+                           lap[h]);
+          }
+        } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        out[j] = star_finish(p, lap[j], f4get(w[R], j), f4get(u2v, j), f4get(mv, j));
+          for (int h = 0; h < 2; ++h) {
+            const int lo = T::OFF + 2 * h - k, hi = T::OFF + 2 * h + k;
+            const float l0 = __fmaf_rn(p.c[2][k], __fadd_rn(zw[lo], zw[hi]), v2lo(lap[h]));
+            const float l1 = __fmaf_rn(p.c[2][k], __fadd_rn(zw[lo + 1], zw[hi + 1]), v2hi(lap[h]));
+            lap[h] = v2pack(l0, l1);
+          }
+        }
+      }
+      float out[4];
+      if (p.m == nullptr || p.m_is_scale) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const V2 sc = p.m == nullptr ? v2bcast(p.C) : f4pair(mv, h);
+          V2 t = vcmul(p.A, f4pair(wv(R), h));
+          t = vcfma(p.B, f4pair(u2v, h), t);
+          const V2 o = vfma(sc, lap[h], t);
+          out[2 * h] = v2lo(o);
+          out[2 * h + 1] = v2hi(o);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          out[2 * h] = star_finish(p, v2lo(lap[h]), f4get(wv(R), 2 * h), f4get(u2v, 2 * h),
+                                   f4get(mv, 2 * h));
+          out[2 * h + 1] = star_finish(p, v2hi(lap[h]), f4get(wv(R), 2 * h + 1),
+                                       f4get(u2v, 2 * h + 1), f4get(mv, 2 * h + 1));
+        }
+      }
       __stcs(reinterpret_cast<float4*>(p.u1 + (int64_t)x * sx + col),
              make_float4(out[0], out[1], out[2], out[3]));
       // fused halo push: this float4 also lands in every neighbour HALO
@@ -393,8 +438,39 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[s]);
+  };
+
+  if constexpr (kStarRing<R>) {
+    // register ring: unrolled by W, slot indices are constants (no moves)
+    for (int i0 = 0; i0 < nit; i0 += W) {
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        const int i = i0 + j;
+        if (i < nit) {
+          const int s = i % T::S;
+          mbar_wait(&full_bar[s], (i / T::S) & 1);
+          const unsigned char* st = sm + s * T::STAGE;
+          w[j] = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(st) +
+                                                  warp * kTZ + 4 * lane);
+          consume(i, j, st);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar[s]);
+        }
+      }
+    }
+  } else {
+    for (int i = 0; i < nit; ++i) {
+      const int s = i % T::S;
+      mbar_wait(&full_bar[s], (i / T::S) & 1);
+      const unsigned char* st = sm + s * T::STAGE;
+#pragma unroll
+      for (int k = 0; k < 2 * R; ++k) w[k] = w[k + 1];
+      w[2 * R] = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(st) +
+                                                  warp * kTZ + 4 * lane);
+      consume(i, W - 1, st);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
   }
 }
 
@@ -472,6 +548,10 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
   p.u0 = u0; p.u2 = (B == 0.0f) ? nullptr : u2; p.m = m; p.u1 = u1;
   p.m_is_scale = (variant & SDMP_VARIANT_M_IS_SCALE) ? 1 : 0;
   variant &= 0xff;
+  if (variant == 0) {  // SDMP_STAR_VARIANT: development A/B of the launch shapes
+    static const int env_variant = getenv("SDMP_STAR_VARIANT") ? atoi(getenv("SDMP_STAR_VARIANT")) : 0;
+    variant = env_variant;
+  }
   float cs = 0.f;
   for (int a = 0; a < 3; ++a) {
     SDMP_CHECK(radius[a] >= 0 && radius[a] <= SDMP_MAX_RADIUS, "radius outside 0..8");

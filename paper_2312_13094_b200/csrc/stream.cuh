@@ -37,7 +37,7 @@ constexpr int kSZ = 32;  // lanes along z
 
 __host__ __device__ constexpr int sround4(int r) { return (r + 3) & ~3; }
 
-template <int R, int TY, int V, int NF, int NC, int NP>
+template <int R, int TY, int V, int NF, int NC, int NP, int CT = 1>
 struct SLayout {
   static constexpr int TZ = kSZ * V;
   static constexpr int OFF = sround4(R);
@@ -46,7 +46,7 @@ struct SLayout {
   static constexpr int FRONT = TZ * TY * 4;
   static constexpr int CENTER = ((CZ * CY * 4) + 127) & ~127;
   static constexpr int STAGE = NF * FRONT + NC * CENTER + NP * FRONT;
-  static constexpr int S0 = (220 * 1024) / STAGE;
+  static constexpr int S0 = (220 * 1024) / CT / STAGE;  // CT resident CTAs per SM
   static constexpr int S = S0 > 4 ? 4 : (S0 < 2 ? 2 : S0);
   static constexpr int BYTES = S * STAGE + 2 * S * 8;
   static constexpr int THREADS = 32 * (TY + 1);
@@ -70,6 +70,17 @@ struct RingOf<Op, std::void_t<decltype(Op::kRing)>> {
 #define SDMP_RING 1
 #endif
   static constexpr bool value = SDMP_RING && Op::kRing;
+};
+
+// Op::kCtas (optional, default 1): resident CTAs per SM (launch bounds and
+// the shared-memory ring are sized for it)
+template <class Op, class = void>
+struct CtasOf {
+  static constexpr int value = 1;
+};
+template <class Op>
+struct CtasOf<Op, std::void_t<decltype(Op::kCtas)>> {
+  static constexpr int value = Op::kCtas;
 };
 
 template <int V> struct VType;
@@ -177,11 +188,12 @@ __device__ __forceinline__ void vstore(float* p, int64_t idx, V2 v, bool m0, boo
 }
 
 template <int R, int TY, int V, class Op>
-__global__ void __launch_bounds__(SLayout<R, TY, V, Op::NF, Op::NC, Op::NP>::THREADS, 1)
+__global__ void __launch_bounds__(SLayout<R, TY, V, Op::NF, Op::NC, Op::NP>::THREADS,
+                                  CtasOf<Op>::value)
 stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, const int xchunk,
               const __grid_constant__ Push push) {
   constexpr int NF = Op::NF, NC = Op::NC, NP = Op::NP;
-  using L = SLayout<R, TY, V, NF, NC, NP>;
+  using L = SLayout<R, TY, V, NF, NC, NP, CtasOf<Op>::value>;
   using T = typename VType<V>::T;
   // __align__(1024) keeps TMA destinations aligned without integer pointer
   // arithmetic, so the consumers keep shared-space pointers (LDS)
@@ -298,8 +310,8 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
 }
 
 // x-chunk count: whole waves of one CTA per SM, small priming overhead.
-inline int stream_chunks(int64_t tiles, int nx, int R) {
-  const int64_t slots = (int64_t)num_sms();
+inline int stream_chunks(int64_t tiles, int nx, int R, int ctas = 1) {
+  const int64_t slots = (int64_t)num_sms() * ctas;
   double best = 1e30;
   int best_n = 1;
   for (int n = 1; n <= 64 && n <= nx; ++n) {
@@ -320,7 +332,7 @@ inline int stream_chunks(int64_t tiles, int nx, int R) {
 template <int R, int TY, int V, class Op>
 int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const float* const* ptrs,
                      cudaStream_t st, const Push* push = nullptr) {
-  using L = SLayout<R, TY, V, Op::NF, Op::NC, Op::NP>;
+  using L = SLayout<R, TY, V, Op::NF, Op::NC, Op::NP, CtasOf<Op>::value>;
   static_assert(Op::NF + Op::NC + Op::NP <= kMaxMaps, "too many tensor maps");
   static int attr_dev = -1;
   int dev = 0;
@@ -346,7 +358,7 @@ int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const f
   }
   const int nz = g.hi[2] - g.lo[2], ny = g.hi[1] - g.lo[1], nx = g.hi[0] - g.lo[0];
   const int tz = (nz + (g.lo[2] & 3) + L::TZ - 1) / L::TZ, ty = (ny + TY - 1) / TY;
-  int nch = stream_chunks((int64_t)tz * ty, nx, R);
+  int nch = stream_chunks((int64_t)tz * ty, nx, R, CtasOf<Op>::value);
   const int chunk = (nx + nch - 1) / nch;
   nch = (nx + chunk - 1) / chunk;
   SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");

@@ -12,7 +12,15 @@ VARIANTS = {
     "both": ["SDMP_RING=1", "SDMP_ODD_PAIR=0"],
 }
 if __name__ == "__main__":
-    names = sys.argv[1:] or list(VARIANTS)
+    # name or name=DEF1,DEF2 (ad-hoc variant)
+    names = []
+    for arg in sys.argv[1:] or list(VARIANTS):
+        if "=" in arg and arg.split("=", 1)[0] not in VARIANTS and "," in arg or arg.count("=") >= 2:
+            n, defs = arg.split("=", 1)
+            VARIANTS[n] = defs.split(",")
+            names.append(n)
+        else:
+            names.append(arg)
     root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "abtest")
     os.makedirs(root, exist_ok=True)
     for n in names:
