@@ -53,19 +53,31 @@ __device__ __forceinline__ typename A::T dminus(const A& a, const float* c) {
 
 // ---- per-point routines (shared by both launch shapes) --------------------
 
-template <int R, class A>
-__device__ __forceinline__ void vel_point(const A& a, const ElCoef& k, typename A::T out[3]) {
+// one velocity component: v_C += b dt (Dx + Dy + Dz) with the staggering
+// of component C (x: D+ txx, D- txy, D- txz; y: D- txy, D+ tyy, D- tyz;
+// z: D- txz, D- tyz, D+ tzz)
+template <int R, int C, class A>
+__device__ __forceinline__ typename A::T vel_comp(const A& a, const ElCoef& k) {
   using T = typename A::T;
   const T bdt = vcmul(k.dt, a.template p<PB>());
-  T dvx = vadd(vadd(dplus<R, 0, TXX>(a, k.c[0]), dminus<R, 1, TXY>(a, k.c[1])),
-               dminus<R, 2, TXZ>(a, k.c[2]));
-  T dvy = vadd(vadd(dminus<R, 0, TXY>(a, k.c[0]), dplus<R, 1, TYY>(a, k.c[1])),
-               dminus<R, 2, TYZ>(a, k.c[2]));
-  T dvz = vadd(vadd(dminus<R, 0, TXZ>(a, k.c[0]), dminus<R, 1, TYZ>(a, k.c[1])),
-               dplus<R, 2, TZZ>(a, k.c[2]));
-  out[0] = vfma(bdt, dvx, a.template p<VX>());
-  out[1] = vfma(bdt, dvy, a.template p<VY>());
-  out[2] = vfma(bdt, dvz, a.template p<VZ>());
+  T d;
+  if constexpr (C == 0)
+    d = vadd(vadd(dplus<R, 0, TXX>(a, k.c[0]), dminus<R, 1, TXY>(a, k.c[1])),
+             dminus<R, 2, TXZ>(a, k.c[2]));
+  else if constexpr (C == 1)
+    d = vadd(vadd(dminus<R, 0, TXY>(a, k.c[0]), dplus<R, 1, TYY>(a, k.c[1])),
+             dminus<R, 2, TYZ>(a, k.c[2]));
+  else
+    d = vadd(vadd(dminus<R, 0, TXZ>(a, k.c[0]), dminus<R, 1, TYZ>(a, k.c[1])),
+             dplus<R, 2, TZZ>(a, k.c[2]));
+  return vfma(bdt, d, a.template p<VX + C>());
+}
+
+template <int R, class A>
+__device__ __forceinline__ void vel_point(const A& a, const ElCoef& k, typename A::T out[3]) {
+  out[0] = vel_comp<R, 0>(a, k);
+  out[1] = vel_comp<R, 1>(a, k);
+  out[2] = vel_comp<R, 2>(a, k);
 }
 
 // strains from v (logical VX, VY, VZ): exx, eyy, ezz, exy, exz, eyz
