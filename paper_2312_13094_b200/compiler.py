@@ -617,7 +617,13 @@ def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
         elif mode == "diagonal":
             msgs = diagonal_messages(decomp, rank, spot.radius)
             acts.append(Action("post", 2, phase=epoch, spot=spot, messages=msgs))
-            acts.append(Action("wait", 0, phase=epoch, spot=spot, messages=msgs))
+            # the wait follows the post on the exchange stream (a spinning
+            # wait on the compute stream, unordered with the post, replays
+            # ~1.7x slower inside CUDA graphs: measured r02)
+            acts.append(Action("wait", 2, phase=epoch, spot=spot, messages=msgs))
+            acts.append(Action("record", 2, event=ev))
+            acts.append(Action("streamwait", 0, event=ev))
+            ev += 1
             epoch += 1
             for t in my_interps:
                 acts.append(Action("interp", 0, sparse=t))

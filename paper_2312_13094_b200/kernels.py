@@ -61,7 +61,7 @@ def _vp_law(gx, gy, gz, nz, vmin=1.5, vmax=4.5, noise=0.01, seed=0):
     return base * (1.0 + noise * (2.0 * u - 1.0))
 
 
-def _fill(fns: Sequence[Function], f, max_points: int = 1 << 25):
+def _fill(fns: Sequence[Function], f, max_points: int = 1 << 27):
     """Write ``f(gx, gy, gz)`` (a tuple of fp64 tensors, one per field) into
     the DOMAIN of each static field, slab by slab along x so the fp64 /
     int64 temporaries stay bounded (a 1536^3 TTI rank would otherwise need
