@@ -594,9 +594,15 @@ def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
                       and t not in [a.sparse for a in acts if a.kind == "interp"]]
         my_injects = [t for t in injects if kernel_writes_field(k, t.field)]
         if spot is not None:
-            # the exchange stream must see this step's previous compute
+            # the exchange stream must see this step's previous compute; in
+            # full mode so must the remainder stream: its OWNED kernels read
+            # values next to CORE that the previous phase's CORE kernel (and
+            # the injection) wrote on stream 0, and the peer's flag does not
+            # order them (found by the full-size bitwise check, r02)
             acts.append(Action("record", 0, event=ev))
             acts.append(Action("streamwait", 2, event=ev))
+            if mode == "full":
+                acts.append(Action("streamwait", 1, event=ev))
             ev += 1
         if spot is None:
             for t in my_interps:
