@@ -57,7 +57,17 @@ def elastic(grid, tag, steps, so=8, visco=False):
     kd.fields["txx"].data[:] = t0
     dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.1)))
     names = KD.VNAMES + KD.TNAMES
-    return Operator([kd]), dt, [kd.fields[n] for n in names], None
+    # a source on a rank boundary (its injection is pushed into the
+    # neighbour's halo in full mode) and receivers crossing ranks
+    ext = grid.extent
+    src = KD.point_source(grid, [(0.5 * ext[0] + 0.3, 0.5 * ext[1] + 0.2, 0.4 * ext[2])], steps, dt,
+                          f0=0.03, name=f"src{tag}")
+    rc = np.stack([np.linspace(5.0, ext[0] - 5.0, 9), np.full(9, 0.5 * ext[1]),
+                   np.full(9, 0.3 * ext[2])], 1)
+    rec = SparseTimeFunction(f"rec{tag}", grid, 9, steps, coordinates=rc)
+    op = Operator([kd, src.inject(kd.fields["txx"].forward, expr=src * S.DT),
+                   rec.interpolate(kd.fields["vz"])])
+    return op, dt, [kd.fields[n] for n in names], rec
 
 
 def main():
