@@ -315,7 +315,10 @@ def main():
     big_i, big_a = max(comp, key=lambda ia: rows[plan.native_index[ia[0]]][4])
     big_pts = math.prod(h_ - l_ for l_, h_ in zip(*big_a.box))
     big_ms = rows[plan.native_index[big_i]][4]
-    kernel_label = {"acoustic": f"star_tma<{args.so // 2}> (acoustic SO-{args.so}, TMA pipeline)",
+    kernel_label = {"acoustic": (f"star_tma<{args.so // 2}> (acoustic SO-{args.so}, TMA pipeline)"
+                                 if args.so < 12 else
+                                 f"star_tma2<{args.so // 2}> (acoustic SO-{args.so}, TMA pipeline, "
+                                 "2 rows per thread)"),
                     "tti": f"tti_g + tti_update (SO-{args.so})",
                     "elastic": f"el_velocity / el_stress (SO-{args.so})",
                     "visco": f"el_velocity / visco_stress (SO-{args.so})"}[kname]

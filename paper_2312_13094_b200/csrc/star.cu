@@ -253,6 +253,79 @@ static int launch_stream(const StarParams& p, cudaStream_t st) {
 //   centre [TY+2R][128+2*OFF]   u0 at plane p-R (=x)  -> y/z taps   (i >= 2R)
 //   u2, m  [TY][128]            at plane x                          (i >= 2R)
 
+// ---- pieces shared by the TMA star kernels (one row of 4 z points) -------
+
+// z taps of one row: zw = the row's z neighbourhood (OFF floats each side)
+template <int R, int OFF>
+__device__ __forceinline__ void star_ztaps(const StarParams& p, const float* zw, V2 lap[2]) {
+#pragma unroll
+  for (int k = 1; k <= R; ++k) {
+    if ((k & 1) == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int lo = OFF + 2 * h - k, hi = OFF + 2 * h + k;
+        lap[h] = vcfma(p.c[2][k], vadd(v2pack(zw[lo], zw[lo + 1]), v2pack(zw[hi], zw[hi + 1])),
+                       lap[h]);
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int lo = OFF + 2 * h - k, hi = OFF + 2 * h + k;
+        const float l0 = __fmaf_rn(p.c[2][k], __fadd_rn(zw[lo], zw[hi]), v2lo(lap[h]));
+        const float l1 = __fmaf_rn(p.c[2][k], __fadd_rn(zw[lo + 1], zw[hi + 1]), v2hi(lap[h]));
+        lap[h] = v2pack(l0, l1);
+      }
+    }
+  }
+}
+
+// u1 = A u0 + B u2 + S lap on 4 points (star_finish per lane)
+__device__ __forceinline__ void star_finish4(const StarParams& p, const V2 lap[2], const float4& c0,
+                                             const float4& u2v, const float4& mv, float out[4]) {
+  if (p.m == nullptr || p.m_is_scale) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const V2 sc = p.m == nullptr ? v2bcast(p.C) : f4pair(mv, h);
+      V2 t = vcmul(p.A, f4pair(c0, h));
+      t = vcfma(p.B, f4pair(u2v, h), t);
+      const V2 o = vfma(sc, lap[h], t);
+      out[2 * h] = v2lo(o);
+      out[2 * h + 1] = v2hi(o);
+    }
+  } else {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      out[2 * h] = star_finish(p, v2lo(lap[h]), f4get(c0, 2 * h), f4get(u2v, 2 * h),
+                               f4get(mv, 2 * h));
+      out[2 * h + 1] = star_finish(p, v2hi(lap[h]), f4get(c0, 2 * h + 1), f4get(u2v, 2 * h + 1),
+                                   f4get(mv, 2 * h + 1));
+    }
+  }
+}
+
+// streaming store of 4 points + fused halo push: the float4 also lands in
+// every neighbour HALO whose receive box contains it
+__device__ __forceinline__ void star_store4(const StarParams& p, const Push& push, int x, int y,
+                                            int z, const float out[4]) {
+  __stcs(reinterpret_cast<float4*>(p.u1 + (int64_t)x * p.g.sx + (int64_t)y * p.g.sy + z),
+         make_float4(out[0], out[1], out[2], out[3]));
+  for (int d = 0; d < push.ndir; ++d) {
+    const PushGeo& pg = push.geo[d];
+    if (x < pg.lo[0] || x >= pg.hi[0] || y < pg.lo[1] || y >= pg.hi[1] || z + 3 < pg.lo[2] ||
+        z >= pg.hi[2])
+      continue;
+    float* dst = push.base[0][d] + (int64_t)(x + pg.off[0]) * pg.psx +
+                 (int64_t)(y + pg.off[1]) * pg.psy + (z + pg.off[2]);
+    if (z >= pg.lo[2] && z + 3 < pg.hi[2] && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+      *reinterpret_cast<float4*>(dst) = make_float4(out[0], out[1], out[2], out[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (z + j >= pg.lo[2] && z + j < pg.hi[2]) dst[j] = out[j];
+    }
+  }
+}
+
 template <int R, int TY>
 struct TmaCfg {
   static constexpr int OFF = round4(R);
@@ -330,8 +403,6 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
 
   const int z = z0 + 4 * lane, y = y0 + warp;
   const bool active = (z < p.g.hi[2]) && (y < p.g.hi[1]);
-  const int64_t sx = p.g.sx, sy = p.g.sy;
-  const int64_t col = (int64_t)y * sy + z;
   constexpr int W = 2 * R + 1;
   float4 w[W];
 #pragma unroll
@@ -379,64 +450,10 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
         for (int h = 0; h < 2; ++h)
           lap[h] = vcfma(p.c[1][k], vadd(f4pair(a, h), f4pair(b, h)), lap[h]);
       }
-#pragma unroll
-      for (int k = 1; k <= R; ++k) {
-        if ((k & 1) == 0) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int lo = T::OFF + 2 * h - k, hi = T::OFF + 2 * h + k;
-            lap[h] = vcfma(p.c[2][k], vadd(v2pack(zw[lo], zw[lo + 1]), v2pack(zw[hi], zw[hi + 1])),
-                           lap[h]);
-          }
-        } else {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int lo = T::OFF + 2 * h - k, hi = T::OFF + 2 * h + k;
-            const float l0 = __fmaf_rn(p.c[2][k], __fadd_rn(zw[lo], zw[hi]), v2lo(lap[h]));
-            const float l1 = __fmaf_rn(p.c[2][k], __fadd_rn(zw[lo + 1], zw[hi + 1]), v2hi(lap[h]));
-            lap[h] = v2pack(l0, l1);
-          }
-        }
-      }
+      star_ztaps<R, T::OFF>(p, zw, lap);
       float out[4];
-      if (p.m == nullptr || p.m_is_scale) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const V2 sc = p.m == nullptr ? v2bcast(p.C) : f4pair(mv, h);
-          V2 t = vcmul(p.A, f4pair(wv(R), h));
-          t = vcfma(p.B, f4pair(u2v, h), t);
-          const V2 o = vfma(sc, lap[h], t);
-          out[2 * h] = v2lo(o);
-          out[2 * h + 1] = v2hi(o);
-        }
-      } else {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          out[2 * h] = star_finish(p, v2lo(lap[h]), f4get(wv(R), 2 * h), f4get(u2v, 2 * h),
-                                   f4get(mv, 2 * h));
-          out[2 * h + 1] = star_finish(p, v2hi(lap[h]), f4get(wv(R), 2 * h + 1),
-                                       f4get(u2v, 2 * h + 1), f4get(mv, 2 * h + 1));
-        }
-      }
-      __stcs(reinterpret_cast<float4*>(p.u1 + (int64_t)x * sx + col),
-             make_float4(out[0], out[1], out[2], out[3]));
-      // fused halo push: this float4 also lands in every neighbour HALO
-      // whose receive box contains it (x/y-split boxes span full z rows)
-      for (int d = 0; d < push.ndir; ++d) {
-        const PushGeo& pg = push.geo[d];
-        if (x < pg.lo[0] || x >= pg.hi[0] || y < pg.lo[1] || y >= pg.hi[1] ||
-            z + 3 < pg.lo[2] || z >= pg.hi[2])
-          continue;
-        float* dst = push.base[0][d] + (int64_t)(x + pg.off[0]) * pg.psx +
-                     (int64_t)(y + pg.off[1]) * pg.psy + (z + pg.off[2]);
-        if (z >= pg.lo[2] && z + 3 < pg.hi[2] && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-          *reinterpret_cast<float4*>(dst) = make_float4(out[0], out[1], out[2], out[3]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (z + j >= pg.lo[2] && z + j < pg.hi[2]) dst[j] = out[j];
-        }
-      }
+      star_finish4(p, lap, wv(R), u2v, mv, out);
+      star_store4(p, push, x, y, z, out);
     }
   };
 
@@ -523,6 +540,179 @@ static int launch_tma(const StarParams& p, cudaStream_t st, const int64_t full[3
   return SDMP_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Wide stencils (R >= 6): the same pipeline with TWO consecutive y rows per
+// consumer thread.  The 2R+2 staged rows a thread needs for both rows' y taps
+// are read from shared memory once (software-pipelined so each row keeps its
+// k-ascending order): 34 instead of 48 LDS.128 per 8 points, and TY = 16 rows
+// per CTA halves the centre tile's y-halo overhead versus one row per warp
+// (the wide stencils are shared-memory-bandwidth bound, profiles/r02).
+
+template <int R, int TY>
+__global__ void __launch_bounds__(32 * (TY / 2 + 1), 1)
+star_tma2(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ CUtensorMap tm_center,
+          const __grid_constant__ CUtensorMap tm_u2, const __grid_constant__ CUtensorMap tm_m,
+          StarParams p, int xchunk, const Push push) {
+  using T = TmaCfg<R, TY>;
+  constexpr int NW = TY / 2;  // consumer warps
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = smraw;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sm + T::S * T::STAGE);
+  uint64_t* empty_bar = full_bar + T::S;
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const bool has_u2 = p.u2 != nullptr, has_m = p.m != nullptr;
+  if (lane == 0 && warp == 0) {
+    for (int s = 0; s < T::S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], NW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int z0 = p.g.lo[2] + blockIdx.x * kTZ;
+  const int y0 = p.g.lo[1] + blockIdx.y * TY;
+  const int xa = p.g.lo[0] + blockIdx.z * xchunk;
+  const int xb = min(xa + xchunk, p.g.hi[0]);
+  const int nit = (xb - xa) + 2 * R;
+
+  if (warp == NW) {  // producer
+    if (lane == 0) {
+      prefetch_tmap(&tm_front);
+      prefetch_tmap(&tm_center);
+      const uint32_t main_bytes =
+          T::FRONT + T::CZ * T::CY * 4 + (has_u2 ? T::FRONT : 0) + (has_m ? T::FRONT : 0);
+      for (int i = 0; i < nit; ++i) {
+        const int s = i % T::S;
+        mbar_wait(&empty_bar[s], ((i / T::S) & 1) ^ 1);
+        unsigned char* st = sm + s * T::STAGE;
+        const bool main = i >= 2 * R;
+        mbar_arrive_expect_tx(&full_bar[s], main ? main_bytes : (uint32_t)T::FRONT);
+        tma_load_3d(st, &tm_front, &full_bar[s], z0, y0, xa - R + i);
+        if (main) {
+          const int x = xa + i - 2 * R;
+          tma_load_3d(st + T::FRONT, &tm_center, &full_bar[s], z0 - T::OFF, y0 - R, x);
+          if (has_u2) tma_load_3d(st + T::FRONT + T::CENTER, &tm_u2, &full_bar[s], z0, y0, x);
+          if (has_m)
+            tma_load_3d(st + 2 * T::FRONT + T::CENTER, &tm_m, &full_bar[s], z0, y0, x);
+        }
+      }
+    }
+    return;
+  }
+
+  const int z = z0 + 4 * lane, r0 = 2 * warp;  // rows r0, r0 + 1 of the tile
+  const bool zin = z < p.g.hi[2];
+  const bool act0 = zin && (y0 + r0 < p.g.hi[1]), act1 = zin && (y0 + r0 + 1 < p.g.hi[1]);
+  constexpr int W = 2 * R + 1;
+  float4 w0[W], w1[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) w0[k] = w1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  for (int i = 0; i < nit; ++i) {
+    const int s = i % T::S;
+    mbar_wait(&full_bar[s], (i / T::S) & 1);
+    const unsigned char* st = sm + s * T::STAGE;
+    const float* front = reinterpret_cast<const float*>(st) + 4 * lane;
+#pragma unroll
+    for (int k = 0; k < 2 * R; ++k) {
+      w0[k] = w0[k + 1];
+      w1[k] = w1[k + 1];
+    }
+    w0[2 * R] = *reinterpret_cast<const float4*>(front + r0 * kTZ);
+    w1[2 * R] = *reinterpret_cast<const float4*>(front + (r0 + 1) * kTZ);
+    if (i >= 2 * R && (act0 || act1)) {
+      const int x = xa + i - 2 * R;
+      // centre tile row (r0 + R + d) at this thread's 4 z points
+      const float* crow = reinterpret_cast<const float*>(st + T::FRONT) + (r0 + R) * T::CZ +
+                          T::OFF + 4 * lane;
+      auto rowv = [&](int d) { return *reinterpret_cast<const float4*>(crow + d * T::CZ); };
+      V2 l0[2], l1[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        l0[h] = vcmul(p.csum0, f4pair(w0[R], h));
+        l1[h] = vcmul(p.csum0, f4pair(w1[R], h));
+      }
+#pragma unroll
+      for (int k = 1; k <= R; ++k)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          l0[h] = vcfma(p.c[0][k], vadd(f4pair(w0[R - k], h), f4pair(w0[R + k], h)), l0[h]);
+          l1[h] = vcfma(p.c[0][k], vadd(f4pair(w1[R - k], h), f4pair(w1[R + k], h)), l1[h]);
+        }
+      // y taps: row 0 uses rows -k / +k, row 1 rows 1-k / 1+k (k ascending
+      // for each): A_k = row(-k), B_k = row(+k); row 1 at k takes
+      // A_{k-1} (A_0 = row 0) and B_{k+1}, loaded one step ahead
+      float4 am = rowv(0), bk = rowv(1), bn;
+#pragma unroll
+      for (int k = 1; k <= R; ++k) {
+        const float4 ak = rowv(-k);
+        bn = rowv(k + 1);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          l0[h] = vcfma(p.c[1][k], vadd(f4pair(ak, h), f4pair(bk, h)), l0[h]);
+          l1[h] = vcfma(p.c[1][k], vadd(f4pair(am, h), f4pair(bn, h)), l1[h]);
+        }
+        am = ak;
+        bk = bn;
+      }
+      constexpr int NZW = (4 + 2 * T::OFF) / 4;
+      float zw[4 * NZW];
+      float out[4];
+      const float* pts = reinterpret_cast<const float*>(st + T::FRONT + T::CENTER) + 4 * lane;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float* zr = crow + j * T::CZ - T::OFF;
+#pragma unroll
+        for (int q = 0; q < NZW; ++q) {
+          const float4 v = *reinterpret_cast<const float4*>(zr + 4 * q);
+          zw[4 * q + 0] = v.x; zw[4 * q + 1] = v.y; zw[4 * q + 2] = v.z; zw[4 * q + 3] = v.w;
+        }
+        V2* l = j == 0 ? l0 : l1;
+        star_ztaps<R, T::OFF>(p, zw, l);
+        const int rr = r0 + j;
+        const float4 u2v = has_u2 ? *reinterpret_cast<const float4*>(pts + rr * kTZ)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 mv = has_m ? *reinterpret_cast<const float4*>(pts + T::FRONT / 4 + rr * kTZ)
+                                : make_float4(1.f, 1.f, 1.f, 1.f);
+        star_finish4(p, l, j == 0 ? w0[R] : w1[R], u2v, mv, out);
+        if (j == 0 ? act0 : act1) star_store4(p, push, x, y0 + rr, z, out);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
+  }
+}
+
+template <int R, int TY>
+static int launch_tma2(const StarParams& p, cudaStream_t st, const int64_t full[3],
+                       const Push& push) {
+  using T = TmaCfg<R, TY>;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    SDMP_CUDA(cudaFuncSetAttribute(star_tma2<R, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   T::BYTES));
+    attr_dev = dev;
+  }
+  CUtensorMap tf, tc, t2, tm;
+  int rc = make_tmap_3d(&tf, p.u0, full, kTZ, TY, false);
+  if (!rc) rc = make_tmap_3d(&tc, p.u0, full, T::CZ, T::CY, false);
+  if (!rc) rc = make_tmap_3d(&t2, p.u2 ? p.u2 : p.u0, full, kTZ, TY, true);
+  if (!rc) rc = make_tmap_3d(&tm, p.m ? p.m : p.u0, full, kTZ, TY, true);
+  if (rc) return rc;
+  const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
+  const int tz = (nz + kTZ - 1) / kTZ, ty = (ny + TY - 1) / TY;
+  int nch = pick_chunks((int64_t)tz * ty, nx, R, 1);
+  const int chunk = (nx + nch - 1) / nch;
+  nch = (nx + chunk - 1) / chunk;
+  SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");
+  dim3 grid(tz, ty, nch), block(32, TY / 2 + 1);
+  star_tma2<R, TY><<<grid, block, T::BYTES, st>>>(tf, tc, t2, tm, p, chunk, push);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
 static int launch_generic(const StarParams& p, cudaStream_t st, const Push& push) {
   const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
   SDMP_CHECK(nx <= 65535, "generic kernel: box x extent > 65535");
@@ -579,6 +769,22 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
       case 6: return launch_stream<6>(p, st);
       case 7: return launch_stream<7>(p, st);
       case 8: return launch_stream<8>(p, st);
+    }
+  }
+  // wide stencils: two rows per thread.  16-row tiles (9 warps: ptxas caps
+  // registers at 168) while the two x-windows fit; R = 8 needs ~210
+  // registers, so 12 / 14-row tiles (<= 8 warps, 255 registers)
+  if (variant == 0 || variant == 6) {
+    switch (R) {
+      case 6: return launch_tma2<6, 16>(p, st, full, push);
+      case 7: return launch_tma2<7, 16>(p, st, full, push);
+      case 8: return launch_tma2<8, 14>(p, st, full, push);
+    }
+  }
+  if (variant == 7) {  // A/B
+    switch (R) {
+      case 7: return launch_tma2<7, 14>(p, st, full, push);
+      case 8: return launch_tma2<8, 12>(p, st, full, push);
     }
   }
   switch (R) {  // variant 0 (auto) / 3: TMA pipeline
