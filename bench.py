@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--nrec", type=int, default=256)
     ap.add_argument("--kernel", default="acoustic", choices=["acoustic", "tti", "elastic", "visco"])
     ap.add_argument("--shape", default=None, help="override the global shape nx,ny,nz")
+    ap.add_argument("--topology", default=None,
+                    help="override the rank grid px,py,pz (default 1,1,1 / 2,1,1 / 2,2,1 / 4,2,1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -228,7 +230,9 @@ def main():
     N = ctx.size
     if N not in TOPOS:
         raise SystemExit(f"unsupported GPU count {N}")
-    topo = TOPOS[N]
+    topo = TOPOS[N] if not args.topology else tuple(int(x) for x in args.topology.split(","))
+    if math.prod(topo) != N:
+        raise SystemExit(f"topology {topo} does not match {N} ranks")
     n = args.n
     shape = tuple(n * p for p in topo)
     if args.shape:

@@ -36,6 +36,15 @@ def test_two_gpus_all_families(topo, shape):
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
                     reason="needs >= 4 GPUs")
+def test_four_gpus_x_interior_ranks():
+    # (4,1,1): interior ranks with both x neighbours, as in the 8-GPU (4,2,1) layout
+    rc, rep, err = _run(4, "4,1,1", "64,36,32", "acoustic,tti,elastic,visco")
+    assert rc == 0, (rep, err)
+    assert all(v["equal"] for v in rep["results"].values()), rep
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
+                    reason="needs >= 4 GPUs")
 def test_four_gpus_xy_split():
     rc, rep, err = _run(4, "2,2,1", "44,40,32", "acoustic,tti,elastic,visco")
     assert rc == 0, (rep, err)
