@@ -241,8 +241,14 @@ static int launch_tti_stream(const Op& op, const Geom& g, const int64_t full[3],
     if (ny <= 4) return launch_stream_op<R, 4, 2>(op, g, full, arrs, st, push);
     return launch_stream_op<R, 16, 2>(op, g, full, arrs, st, push);
   } else if constexpr (R <= 4) {
+#ifndef SDMP_GOP_TY
+#define SDMP_GOP_TY 16
+#endif
+#ifndef SDMP_UOP_TY
+#define SDMP_UOP_TY 12
+#endif
     if (ny <= 8) return launch_stream_op<R, 8, 2>(op, g, full, arrs, st, push);
-    return launch_stream_op<R, upd ? 12 : 16, 2>(op, g, full, arrs, st, push);
+    return launch_stream_op<R, upd ? SDMP_UOP_TY : SDMP_GOP_TY, 2>(op, g, full, arrs, st, push);
   } else if constexpr (!upd || R == 5) {
     return launch_stream_op<R, 8, 2>(op, g, full, arrs, st, push);
   } else {

@@ -27,13 +27,13 @@ __device__ __forceinline__ V2 v2pack(float a, float b) {
   return o;
 }
 __device__ __forceinline__ float v2lo(V2 v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v.r));
+  float a;
+  asm("mov.b64 {%0, _}, %1;" : "=f"(a) : "l"(v.r));
   return a;
 }
 __device__ __forceinline__ float v2hi(V2 v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v.r));
+  float b;
+  asm("mov.b64 {_, %0}, %1;" : "=f"(b) : "l"(v.r));
   return b;
 }
 __device__ __forceinline__ V2 v2bcast(float a) { return v2pack(a, a); }

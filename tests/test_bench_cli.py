@@ -60,3 +60,11 @@ def test_run_benchmark_deterministic_and_verified(kernel, shape, so):
     assert a.max_diff == 0.0
     assert a.gpts_per_s == pytest.approx(
         (shape[0] * shape[1] * (shape[2] if len(shape) > 2 else 1)) * 9 / a.walltime_s / 1e9)
+
+
+def test_cli_dump_plan(capsys):
+    """`--dump-plan` prints the Listing-6/7-style tree (host only, no GPU)."""
+    rc = BC.main(["--kernel", "acoustic", "--shape", "24,20,16", "--so", "4", "--mode", "full",
+                  "--dump-plan"])
+    out = capsys.readouterr().out
+    assert rc == 0 and "<Callable Kernel>" in out and "Iteration time" in out
