@@ -166,6 +166,9 @@ int sdmp_plan_add_action(sdmp_plan* plan, const int64_t* ints, int32_t nints,
 /* Run time_m..time_M (inclusive) ordered after / before
  * `stream`.  Asynchronous. */
 int sdmp_plan_run(sdmp_plan* plan, int64_t time_m, int64_t time_M, void* stream);
+/* One timestep (= sdmp_plan_run(plan, time, time, stream)); the SURVEY's
+ * proposed `sdmp_step` for per-step instrumentation. */
+int sdmp_plan_step(sdmp_plan* plan, int64_t time, void* stream);
 /* Block until the plan's streams drain; checks the halo watchdog. */
 int sdmp_plan_sync(sdmp_plan* plan);
 /* Per-action instrumentation: enable (records CUDA events around every

@@ -13,8 +13,8 @@ Drop-in surfaces:
 from . import symbolics
 from .symbolics import (Eq, FieldSpec, GridSpec, StencilEquation, apply_cse, discretize,
                         fd_coefficients, solve_forward)
-from .api import (Data, Function, Grid, Operator, SparseTimeFunction, TimeFunction, ricker,
-                  solve)
+from .api import (Data, Function, Grid, Operator, SparseTimeFunction, TimeFunction, load_dump,
+                  ricker, solve)
 from .decomposition import Decomposition, Topology, default_topology, decompose_axis
 from .distfield import RegionName, region_boxes
 

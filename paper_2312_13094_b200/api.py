@@ -206,6 +206,18 @@ class Data:
             out[tuple(slice(x, y) for x, y in ext)] = a
         return out
 
+    def dump(self, path: str, buffer: Optional[int] = None) -> None:
+        """Gather and write the global field: one text header
+        line ``field=<name> shape=<n0>,<n1>[,<n2>] dtype=float64 order=C``,
+        then the values as row-major 64-bit floats.  Collective; rank 0
+        writes."""
+        out = self.gather(buffer)
+        if self.fn.grid.ctx.rank == 0:
+            with open(path, "wb") as f:
+                shape = ",".join(str(n) for n in out.shape)
+                f.write(f"field={self.fn.name} shape={shape} dtype=float64 order=C\n".encode())
+                f.write(np.ascontiguousarray(out, dtype="<f8").tobytes())
+
     def __array__(self, dtype=None):
         a = self[...]
         return a.astype(dtype) if dtype is not None else a
@@ -322,6 +334,16 @@ class TimeFunction(Function):
             raise ValueError("TimeFunction time_order must be 1 or 2")
         super().__init__(name, grid, space_order=space_order, halo=halo,
                          time_order=time_order)
+
+
+def load_dump(path: str):
+    """Read a :meth:`Data.dump` file -> (field name, float64 array)."""
+    with open(path, "rb") as f:
+        header = f.readline().decode().split()
+        meta = dict(kv.split("=", 1) for kv in header)
+        shape = tuple(int(n) for n in meta["shape"].split(","))
+        data = np.frombuffer(f.read(), dtype="<f8").reshape(shape)
+    return meta["field"], data
 
 
 def field_of(spec: S.FieldSpec) -> Function:
@@ -573,4 +595,4 @@ class Operator:
 
 
 __all__ = ["Grid", "Function", "TimeFunction", "SparseTimeFunction", "Operator", "Eq",
-           "solve", "ricker", "Data", "StencilEquation", "solve_forward"]
+           "solve", "ricker", "Data", "StencilEquation", "solve_forward", "load_dump"]

@@ -757,6 +757,10 @@ extern "C" int sdmp_plan_run(sdmp_plan* p, int64_t time_m, int64_t time_M, void*
   return SDMP_OK;
 }
 
+extern "C" int sdmp_plan_step(sdmp_plan* p, int64_t time, void* stream) {
+  return sdmp_plan_run(p, time, time, stream);
+}
+
 extern "C" int sdmp_plan_sync(sdmp_plan* p) {
   SDMP_CHECK(p, "null plan");
   SDMP_CUDA(cudaSetDevice(p->device));

@@ -75,6 +75,7 @@ def _declare(lib):
                                            vp, vp, vp, vp, C.c_int64, C.c_int64, i32p]),
         "sdmp_plan_add_action": (C.c_int, [vp, i64p, C.c_int32, f32p, C.c_int32]),
         "sdmp_plan_run": (C.c_int, [vp, C.c_int64, C.c_int64, vp]),
+        "sdmp_plan_step": (C.c_int, [vp, C.c_int64, vp]),
         "sdmp_plan_sync": (C.c_int, [vp]),
         "sdmp_plan_set_tracing": (C.c_int, [vp, C.c_int32]),
         "sdmp_plan_trace": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int32, i32p]),

@@ -62,8 +62,18 @@ def listing3(rank, world):
     u.data[:] = rnd
     back = u.data_gather()
     point = u.data[2, 3]
+    # gather dump: header + row-major float64, written by rank 0
+    import tempfile
+    from paper_2312_13094_b200 import load_dump
+    from paper_2312_13094_b200.dist import context
+    path = os.path.join(tempfile.gettempdir(), f"sdmp_dump_{os.getppid()}.bin")
+    u.data.dump(path)
+    context().barrier()
+    name, arr = load_dump(path)
+    dump_ok = name == "u" and arr.dtype == np.float64 and np.array_equal(arr, rnd)
     return {"view": view, "gather": g.tolist(), "roundtrip": bool(np.array_equal(back, rnd)),
-            "topology": grid.topology, "point": np.asarray(point).tolist()}
+            "topology": grid.topology, "point": np.asarray(point).tolist(),
+            "dump_ok": bool(dump_ok)}
 
 
 def plans(rank, world):
@@ -102,6 +112,7 @@ def test_listing3_four_ranks():
         assert out[r]["view"] == want[r]
         assert out[r]["topology"] == (2, 2)
         assert out[r]["roundtrip"]
+        assert out[r]["dump_ok"]
     g = np.array(out[0]["gather"])
     assert g[1:3, 1:3].sum() == 4 and g.sum() == 4
     # global point (2,3) lives on rank 3 only: the others see an empty view
