@@ -313,13 +313,21 @@ static int launch_el_stream(const Op& op, const Geom& g, const int64_t full[3],
   // velocity (few operands, many taps) is issue bound: packed pairs; the
   // stress phases (8-15 pointwise operands) are bandwidth bound: one point
   // per thread keeps stages small and the ring deep (measured, r01).
-  constexpr int V = Op::NP <= 4 ? 2 : 1;
+#ifndef SDMP_STRESS_V
+#define SDMP_STRESS_V 1
+#endif
+#ifndef SDMP_STRESS_TYW
+#define SDMP_STRESS_TYW 8
+#endif
+  constexpr int V = Op::NP <= 4 ? 2 : SDMP_STRESS_V;
+  constexpr int TYW = Op::NP <= 4 ? 8 : SDMP_STRESS_TYW;
   const int ny = g.hi[1] - g.lo[1];
   if constexpr (R <= 4) {
     if (ny <= 4) return launch_stream_op<R, 4, V>(op, g, full, arrs, st, &push);
     return launch_stream_op<R, 16, V>(op, g, full, arrs, st, &push);
   } else {
-    return launch_stream_op<R, 8, V>(op, g, full, arrs, st, &push);
+    if (ny <= 8) return launch_stream_op<R, 8, V>(op, g, full, arrs, st, &push);
+    return launch_stream_op<R, TYW, V>(op, g, full, arrs, st, &push);
   }
 }
 
