@@ -739,8 +739,8 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
   p.m_is_scale = (variant & SDMP_VARIANT_M_IS_SCALE) ? 1 : 0;
   variant &= 0xff;
   if (variant == 0) {  // SDMP_STAR_VARIANT: development A/B of the launch shapes
-    static const int env_variant = getenv("SDMP_STAR_VARIANT") ? atoi(getenv("SDMP_STAR_VARIANT")) : 0;
-    variant = env_variant;
+    const char* e = getenv("SDMP_STAR_VARIANT");
+    variant = e ? atoi(e) : 0;
   }
   float cs = 0.f;
   for (int a = 0; a < 3; ++a) {

@@ -28,3 +28,13 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _fresh_field_registry(request):
+    """Each GPU test builds its own fields: start from an empty name registry
+    (field names are unique per (name, grid, space order) within a process)."""
+    if "gpu" in request.keywords:
+        from paper_2312_13094_b200 import api
+        api._FUNCS.clear()
+    yield

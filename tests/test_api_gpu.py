@@ -63,7 +63,7 @@ def run_acoustic(shape, so, steps, mode, tag, nrec=7):
     return grid, u, m, src, rec, float(dt)
 
 
-@pytest.mark.parametrize("so", [4, 8, 16])
+@pytest.mark.parametrize("so", [4, 8, 12, 16])
 def test_acoustic_vs_oracle(so):
     shape, steps = (40, 36, 44), 30
     grid, u, m, src, rec, dt = run_acoustic(shape, so, steps, "diagonal", f"a{so}")
@@ -95,8 +95,9 @@ def test_modes_bitwise_equal_single_rank():
         assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
 
 
-def test_tti_vs_oracle():
-    shape, so, steps = (28, 24, 32), 8, 10
+@pytest.mark.parametrize("so", [4, 8, 12, 16])
+def test_tti_vs_oracle(so):
+    shape, steps = (28, 24, 32), 10
     grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
     kd = KD.tti_model(grid, so=so)
     p, r = kd.fields["p"], kd.fields["r"]
@@ -125,10 +126,10 @@ def test_tti_vs_oracle():
         assert err <= REL, (name, err, np.abs(got - want).max())
 
 
-@pytest.mark.parametrize("visco", [False, True])
-def test_elastic_vs_oracle(visco):
+@pytest.mark.parametrize("visco,so", [(False, 4), (False, 8), (False, 12), (False, 16),
+                                     (True, 4), (True, 8), (True, 16)])
+def test_elastic_vs_oracle(visco, so):
     shape, steps = (24, 28, 20), 8
-    so = 16 if visco else 8
     grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
     kd = KD.viscoelastic_model(grid, so=so) if visco else KD.elastic_model(grid, so=so)
     rng = np.random.default_rng(1)
@@ -153,6 +154,22 @@ def test_elastic_vs_oracle(visco):
         got = kd.fields[name].data_gather()
         err = rel_l2(got, want)
         assert err <= REL, (name, err, np.abs(got - want).max())
+
+
+@pytest.mark.parametrize("so", [4, 8, 12, 16])
+def test_star_kernels_bitwise_equal_generic(so, monkeypatch):
+    """star_tma (one row per warp), star_tma2 (two rows per thread, SO >= 12)
+    and the generic kernel give identical bits."""
+    outs = []
+    for variant in ("1", "0", "3"):
+        monkeypatch.setenv("SDMP_STAR_VARIANT", variant)
+        import paper_2312_13094_b200.api as A
+        A._FUNCS.clear()
+        _g, u, _m, _s, rec, _dt = run_acoustic((40, 36, 44), so, 8, "diagonal", f"sb{so}_{variant}")
+        outs.append((u.data_gather(), rec.data.copy()))
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
+    assert np.abs(outs[0][0]).max() > 0
 
 
 @pytest.mark.parametrize("family,so", [("tti", 8), ("tti", 12), ("elastic", 8), ("elastic", 4),
