@@ -67,6 +67,19 @@ int sdmp_star_update(void* stream, const float* u0, const float* u2, const float
                      const int64_t hi[3], const int32_t radius[3], const float* coeffs,
                      float A, float B, float C, int32_t variant);
 
+/* Variable-coefficient star (acoustic with an absorbing / damping layer and
+ * other updates whose coefficients depend on static fields):
+ *   u1 = A u0 + B u2 + S L(u0)
+ * with per-point A, B, S arrays (FULL-shaped like u, read at the output
+ * point; B may be NULL, then u2 is unused).  Replaces compute(box, eq) for
+ * the reference's solved `m*u.dt2 - u.laplace + damp*u.dt` (symbolics.py
+ * solve_forward); coefficients are bound once per apply by the
+ * host from the solved update.  variant 1 forces the generic kernel. */
+int sdmp_var_star_update(void* stream, const float* u0, const float* u2, const float* A,
+                         const float* B, const float* S, float* u1, const int64_t full[3],
+                         const int64_t lo[3], const int64_t hi[3], const int32_t radius[3],
+                         const float* coeffs, int32_t variant);
+
 /* Bind a derived fp32 parameter once at plan build:
  * out[i] = in[i] != 0 ? C / in[i] : 0 for n elements (e.g. S = dt^2/m). */
 int sdmp_bind_scale(void* stream, float* out, const float* in, int64_t n, float C);
@@ -139,7 +152,7 @@ typedef struct sdmp_plan sdmp_plan;
 
 enum {
     SDMP_ACT_STAR = 1, SDMP_ACT_TTI = 2, SDMP_ACT_EL_V = 3, SDMP_ACT_EL_T = 4,
-    SDMP_ACT_VISCO_T = 5, SDMP_ACT_INJECT = 6, SDMP_ACT_INTERP = 7,
+    SDMP_ACT_VISCO_T = 5, SDMP_ACT_INJECT = 6, SDMP_ACT_INTERP = 7, SDMP_ACT_VSTAR = 8,
     SDMP_ACT_POST = 10, SDMP_ACT_WAIT = 11, SDMP_ACT_RECORD = 12, SDMP_ACT_STREAMWAIT = 13,
     SDMP_ACT_PACK = 14, SDMP_ACT_UNPACK = 15
 };

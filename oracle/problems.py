@@ -120,6 +120,27 @@ def star(nd, so, coeffs, A, B, C, with_m, sparse=None, shape=None, dims=None, ha
     return Problem(fields, halo, [Phase([("u", 0)], (r,) * nd, compute, before, after)])
 
 
+def var_star(nd, so, coeffs, with_prev=True, sparse=None, shape=None, dims=None, extra=()):
+    """Variable-coefficient star (damped acoustic): static fields A, B, S
+    (+ ``extra`` static fields, e.g. m for the source scaling)."""
+    r = so // 2
+    halo = (so,) * nd
+    fields = {"u": 3 if with_prev else 2, "A": 1, "S": 1}
+    fields.update({n: 1 for n in extra})
+    if with_prev:
+        fields["B"] = 1
+
+    def compute(rk, box, time):
+        b = lambda n, t=0: rk.buf(n, time, t)
+        K.var_star_update(b("u"), b("u", -1) if with_prev else None, b("A"),
+                          b("B") if with_prev else None, b("S"), coeffs, box, b("u", 1))
+
+    before = after = None
+    if sparse is not None:
+        before, after = _sparse_hooks(shape, dims or (1,) * nd, sparse)
+    return Problem(fields, halo, [Phase([("u", 0)], (r,) * nd, compute, before, after)])
+
+
 def tti(so, lap_c, d1_c, dt2, sparse=None, shape=None, dims=None):
     halo = (so,) * 3
     fields = {"p": 3, "r": 3, "m": 1, "epsp": 1, "delp": 1, "ax": 1, "ay": 1, "az": 1}

@@ -53,6 +53,20 @@ def star_update(u0, u2, m, coeffs, A, B, C, box, out):
     out[s] = val
 
 
+def var_star_update(u0, u2, A, B, S, coeffs, box, out):
+    """u1 = A u0 + B u2 + S L(u0) with pointwise coefficient arrays: the
+    reference's solved ``m*u.dt2 - u.laplace + damp*u.dt`` (forward
+    first-order time difference, symbolics.py:530-546, solved by
+    solve_forward, symbolics.py:591-674) gives A = (2m + d dt)/(m + d dt),
+    B = -m/(m + d dt), S = dt^2/(m + d dt).  B None -> no u2 term."""
+    s = _sl(box)
+    lap = star_laplacian(u0, box, coeffs)
+    val = A[s] * u0[s] + S[s] * lap
+    if B is not None:
+        val = val + B[s] * u2[s]
+    out[s] = val
+
+
 def first_derivative(f, box, a, w1):
     """Central first derivative along a with weights w1[k], k=1..R (already
     divided by h): sum_k w_k (f[+k] - f[-k])."""

@@ -89,6 +89,77 @@ class StarKernel:
         return 4 * (2 + (1 if self.B != 0 else 0) + (1 if self.m is not None else 0))
 
 
+@dataclass(eq=False)
+class VarStarKernel:
+    """u1 = A(x) u0 + B(x) u2 + S(x) L(u0) with pointwise coefficients that
+    are functions of static fields and dt — e.g. the acoustic equation with an
+    absorbing (damping) layer, ``m*u.dt2 - u.laplace + damp*u.dt``, which the
+    reference's symbolics solve to A = (2m + d dt)/(m + d dt),
+    B = -m/(m + d dt), S = dt^2/(m + d dt).  A, B, S are evaluated from the
+    solved update itself (``coefficients``) once per apply, in fp64, and
+    bound to fp32 arrays."""
+
+    u: S.FieldSpec
+    statics: Tuple[S.FieldSpec, ...]
+    weights: Tuple[Tuple[Fraction, ...], ...]
+    eq: S.StencilEquation
+    has_prev: bool
+    family: str = "vstar"
+
+    @property
+    def radius(self) -> Tuple[int, ...]:
+        return tuple(len(w) - 1 for w in self.weights)
+
+    def reads(self):
+        out = [(self.u, 0, self.radius)]
+        if self.has_prev:
+            out.append((self.u, -1, (0,) * len(self.radius)))
+        for f in self.statics:
+            out.append((f, 0, (0,) * len(self.radius)))
+        return out
+
+    def writes(self):
+        return [(self.u, 1)]
+
+    @property
+    def bytes_per_point(self) -> int:
+        """u0, u2, A, B, S read, u1 written (the bound coefficient arrays
+        replace the static fields on the hot path)."""
+        return 4 * (2 + (2 if self.has_prev else 1) + 2)
+
+    def coefficients(self, values, dt, spacing):
+        """(A, B, S) from static-field values (arrays of one shape, fp64),
+        dt and the grid spacing, by evaluating the solved update with unit
+        unknowns (it is linear in them)."""
+        u = self.u
+        nd = len(spacing)
+        bind = {}
+        for leaf in _leaves(self.eq.rhs):
+            if isinstance(leaf, S.Symbol):
+                if leaf.name == "dt":
+                    bind[leaf] = float(dt)
+                else:
+                    bind[leaf] = float(spacing[S.AXIS_NAMES.index(leaf.name[2:])])
+            elif leaf.spec in values:
+                bind[leaf] = values[leaf.spec]
+            else:
+                bind[leaf] = 0.0  # the unknowns (u0 taps, u2)
+        centre = S.FieldAccess(u, 0, (0,) * nd)
+        prev = S.FieldAccess(u, -1, (0,) * nd)
+        k1 = S.FieldAccess(u, 0, tuple(1 if b == 0 else 0 for b in range(nd)))
+
+        def coeff(acc):
+            b = dict(bind)
+            b[acc] = 1.0
+            return S.eval_numeric(self.eq.rhs, b)
+
+        W = self.weights
+        Sv = coeff(k1) * (spacing[0] ** 2 / float(W[0][1]))
+        A = coeff(centre) - Sv * sum(float(W[a][0]) / spacing[a] ** 2 for a in range(nd))
+        B = coeff(prev) if self.has_prev else 0.0
+        return A, B, Sv
+
+
 @dataclass
 class TTIKernel:
     """Two-field pseudo-acoustic TTI."""
@@ -286,12 +357,71 @@ def register_family(eq: S.StencilEquation, kernel) -> None:
     _FAMILY_REGISTRY[eq] = kernel
 
 
+def recognise_var_star(eq: S.StencilEquation) -> Optional[VarStarKernel]:
+    """Match u1 = A u0 + B u2 + S L(u0) where A, B, S may depend on any
+    static fields read at the point (exact rational probing with independent
+    random values for every static field; or None)."""
+    u = eq.lhs.spec
+    if u.is_static or eq.lhs.tshift != 1 or any(eq.lhs.offsets) or eq.temporaries:
+        return None
+    accs = S.accesses(eq.rhs)
+    evolving = {a for a in accs if a.spec == u}
+    if any(a.spec != u and (not a.spec.is_static or any(a.offsets)) for a in accs):
+        return None
+    statics = tuple(sorted({a.spec for a in accs if a.spec != u}, key=lambda f: f.name))
+    nd = u.grid.ndims
+    if any(a.tshift not in (0, -1) for a in evolving):
+        return None
+    if any(a.tshift == -1 and any(a.offsets) for a in evolving):
+        return None
+    r = u.space_order // 2
+    weights = [Fraction(w) for w in S.fd_coefficients(2, u.space_order)]
+    W = tuple(weights[r + k] for k in range(r + 1))
+    if W[1] == 0:
+        return None
+    star = {S.FieldAccess(u, 0, tuple(k if b == a else 0 for b in range(nd)))
+            for a in range(nd) for k in range(-r, r + 1)}
+    u0s = {a for a in evolving if a.tshift == 0}
+    if not u0s <= star:
+        return None
+    has_prev = any(a.tshift == -1 for a in evolving)
+    unknowns = sorted(u0s | {a for a in evolving if a.tshift == -1},
+                      key=lambda a: (a.tshift, a.offsets))
+    rng = random.Random(4321)
+    k1 = S.FieldAccess(u, 0, tuple(1 if b == 0 else 0 for b in range(nd)))
+    for _ in range(3):
+        bind = {}
+        hs = [Fraction(rng.randint(2, 40), rng.randint(1, 9)) for _ in range(nd)]
+        svals = {f: Fraction(rng.randint(2, 50), rng.randint(2, 17)) for f in statics}
+        for leaf in _leaves(eq.rhs):
+            if isinstance(leaf, S.Symbol):
+                if leaf.name == "dt":
+                    bind[leaf] = Fraction(rng.randint(2, 30), rng.randint(2, 30))
+                elif leaf.name.startswith("h_"):
+                    bind[leaf] = hs[S.AXIS_NAMES.index(leaf.name[2:])]
+                else:
+                    return None
+            elif leaf.spec != u:
+                bind[leaf] = svals[leaf.spec]
+        co = _coefficients(eq.rhs, unknowns, bind)
+        Sv = co.get(k1, Fraction(0)) * hs[0] ** 2 / W[1]
+        if Sv == 0:
+            return None
+        for a in range(nd):
+            for k in range(1, r + 1):
+                for sgn in (-1, 1):
+                    acc = S.FieldAccess(u, 0, tuple(sgn * k if b == a else 0 for b in range(nd)))
+                    if co.get(acc, Fraction(0)) != Sv * W[k] / hs[a] ** 2:
+                        return None
+    return VarStarKernel(u, statics, tuple(W for _ in range(nd)), eq, has_prev)
+
+
 def recognise(equations: Sequence) -> List[object]:
     """Solved updates -> kernel list (one kernel may own several updates)."""
     kernels: List[object] = []
     seen = set()
     for eq in equations:
-        if isinstance(eq, (StarKernel, TTIKernel, StaggeredPhase)):
+        if isinstance(eq, (StarKernel, VarStarKernel, TTIKernel, StaggeredPhase)):
             kernels.append(eq)
             continue
         if not isinstance(eq, S.StencilEquation):
@@ -304,9 +434,11 @@ def recognise(equations: Sequence) -> List[object]:
             continue
         k = recognise_star(eq)
         if k is None:
+            k = recognise_var_star(eq)
+        if k is None:
             raise CompilerError(
                 "equation not recognised as a supported kernel family (acoustic, "
-                "diffusion, TTI, staggered elastic/viscoelastic): "
+                "damped acoustic, diffusion, TTI, staggered elastic/viscoelastic): "
                 + " ; ".join(S.format_equation(eq))[:300])
         kernels.append(k)
     return kernels

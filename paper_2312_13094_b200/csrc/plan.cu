@@ -33,6 +33,9 @@ const char* get_error() { return g_err.c_str(); }
 int star_update(cudaStream_t, const float*, const float*, const float*, float*, const int64_t*,
                 const int64_t*, const int64_t*, const int32_t*, const float*, float, float, float,
                 int, const Push*);
+int var_star_update(cudaStream_t, const float*, const float*, const float*, const float*,
+                    const float*, float*, const int64_t*, const int64_t*, const int64_t*,
+                    const int32_t*, const float*, int, const Push*);
 int tti_update_entry(cudaStream_t, const float* const*, float*, float*, const int64_t*,
                      const int64_t*, const int64_t*, int32_t, const float*, const float*, float,
                      const Push*);
@@ -140,6 +143,7 @@ constexpr int64_t kPushMagic = -77;
 int base_len(int kind) {
   switch (kind) {
     case SDMP_ACT_STAR: return 19;
+    case SDMP_ACT_VSTAR: return 21;
     case SDMP_ACT_TTI: return 33;
     case SDMP_ACT_EL_V: return 35;
     case SDMP_ACT_EL_T: return 43;
@@ -189,8 +193,8 @@ int parse_push(const sdmp_plan* p, const Action& a, int64_t time, Push* out) {
 // kernel launches).
 int launches_of(const Action& a) {
   switch ((int)a.i[0]) {
-    case SDMP_ACT_STAR: case SDMP_ACT_EL_V: case SDMP_ACT_EL_T: case SDMP_ACT_VISCO_T:
-    case SDMP_ACT_INJECT: case SDMP_ACT_INTERP: case SDMP_ACT_WAIT:
+    case SDMP_ACT_STAR: case SDMP_ACT_VSTAR: case SDMP_ACT_EL_V: case SDMP_ACT_EL_T:
+    case SDMP_ACT_VISCO_T: case SDMP_ACT_INJECT: case SDMP_ACT_INTERP: case SDMP_ACT_WAIT:
       return 1;
     case SDMP_ACT_TTI:
       return 2;
@@ -223,6 +227,18 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       const int nc = 3 * SDMP_NCOEF;
       return star_update(st, u0, u2, m, u1, p->fields[I[2]].full, lo, hi, r, F, F[nc],
                          F[nc + 1], F[nc + 2], (int)I[18], pp);
+    }
+    case SDMP_ACT_VSTAR: {
+      // [k,s, fu0,tu0, fu2,tu2, fA, fB, fS, fu1,tu1, lo3, hi3, r3, variant]
+      const float* u0 = resolve(p, I[2], I[3], time);
+      const float* u2 = resolve(p, I[4], I[5], time);
+      const float* A = resolve(p, I[6], 0, time);
+      const float* B = resolve(p, I[7], 0, time);
+      const float* Sv = resolve(p, I[8], 0, time);
+      float* u1 = resolve(p, I[9], I[10], time);
+      int32_t r[3] = {(int32_t)I[17], (int32_t)I[18], (int32_t)I[19]};
+      return var_star_update(st, u0, u2, A, B, Sv, u1, p->fields[I[2]].full, I + 11, I + 14, r,
+                             F, (int)I[20], pp);
     }
     case SDMP_ACT_TTI: {
       const float* in[10];
@@ -575,7 +591,7 @@ static int validate(const sdmp_plan* p, const Action& a) {
   SDMP_CHECK(I[1] >= 0 && I[1] < 3, "stream id must be 0..2");
   auto fchk = [&](int64_t f) { return f >= -1 && f < (int64_t)p->fields.size(); };
   static const std::map<int, int> min_len = {
-      {SDMP_ACT_STAR, 19}, {SDMP_ACT_TTI, 33}, {SDMP_ACT_EL_V, 35}, {SDMP_ACT_EL_T, 43},
+      {SDMP_ACT_STAR, 19}, {SDMP_ACT_VSTAR, 21}, {SDMP_ACT_TTI, 33}, {SDMP_ACT_EL_V, 35}, {SDMP_ACT_EL_T, 43},
       {SDMP_ACT_VISCO_T, 69}, {SDMP_ACT_INJECT, 6}, {SDMP_ACT_INTERP, 5}, {SDMP_ACT_POST, 6},
       {SDMP_ACT_WAIT, 4}, {SDMP_ACT_RECORD, 3}, {SDMP_ACT_STREAMWAIT, 3}};
   auto it = min_len.find((int)I[0]);
@@ -586,6 +602,12 @@ static int validate(const sdmp_plan* p, const Action& a) {
       SDMP_CHECK(fchk(I[2]) && I[2] >= 0 && fchk(I[4]) && fchk(I[6]) && fchk(I[7]) && I[7] >= 0,
                  "star: field id");
       SDMP_CHECK((int)a.f.size() >= 3 * SDMP_NCOEF + 3, "star: float params");
+      break;
+    case SDMP_ACT_VSTAR:
+      SDMP_CHECK(fchk(I[2]) && I[2] >= 0 && fchk(I[4]) && fchk(I[6]) && I[6] >= 0 &&
+                     fchk(I[7]) && fchk(I[8]) && I[8] >= 0 && fchk(I[9]) && I[9] >= 0,
+                 "vstar: field id");
+      SDMP_CHECK((int)a.f.size() >= 3 * SDMP_NCOEF, "vstar: float params");
       break;
     case SDMP_ACT_INJECT:
       SDMP_CHECK(I[5] >= 0 && I[5] < (int64_t)p->sparse.size(), "inject: set id");

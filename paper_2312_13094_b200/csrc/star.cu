@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "stream.cuh"
 #include "tma.cuh"
 #include "vmath.cuh"
 
@@ -39,22 +40,31 @@ struct StarParams {
   float csum0;  // c_x0 + c_y0 + c_z0 (fp32, host-rounded)
   float A, B, C;
   int m_is_scale;  // m holds the bound scale S = C/m (sdmp_bind_scale)
+  // variable-coefficient family (sdmp_var_star_update): per-point A and B
+  // (B may be null); S comes through m with m_is_scale = 1
+  const float* __restrict__ Av;
+  const float* __restrict__ Bv;
 };
 
 // Shared tail of the per-point update: u1 = A*u0 + B*u2 + S*lap.
 __device__ __forceinline__ float star_finish(const StarParams& p, float lap, float c0, float u2v,
-                                             float mv) {
+                                             float mv, float av, float bv) {
   float s = (p.m == nullptr) ? p.C : (p.m_is_scale ? mv : __fdiv_rn(p.C, mv));
-  float t = __fmul_rn(p.A, c0);
-  t = __fmaf_rn(p.B, u2v, t);
+  float t = __fmul_rn(av, c0);
+  t = __fmaf_rn(bv, u2v, t);
   return __fmaf_rn(s, lap, t);
+}
+__device__ __forceinline__ float star_finish(const StarParams& p, float lap, float c0, float u2v,
+                                             float mv) {
+  return star_finish(p, lap, c0, u2v, mv, p.A, p.B);
 }
 
 // Per-point update.  xs(k)/ys(k)/zs(k) return tap(-k) + tap(+k) along the
 // axis; the sum is formed with __fadd_rn inside the caller.
 template <int RX, int RY, int RZ, class FX, class FY, class FZ>
 __device__ __forceinline__ float star_point(const StarParams& p, float c0, float u2v, float mv,
-                                            int rx, int ry, int rz, FX xs, FY ys, FZ zs) {
+                                            int rx, int ry, int rz, FX xs, FY ys, FZ zs,
+                                            float av, float bv) {
   float lap = __fmul_rn(p.csum0, c0);
 #pragma unroll
   for (int k = 1; k <= (RX > 0 ? RX : SDMP_MAX_RADIUS); ++k)
@@ -65,7 +75,7 @@ __device__ __forceinline__ float star_point(const StarParams& p, float c0, float
 #pragma unroll
   for (int k = 1; k <= (RZ > 0 ? RZ : SDMP_MAX_RADIUS); ++k)
     if (RZ > 0 || k <= rz) lap = __fmaf_rn(p.c[2][k], zs(k), lap);
-  return star_finish(p, lap, c0, u2v, mv);
+  return star_finish(p, lap, c0, u2v, mv, av, bv);
 }
 
 // ---------------------------------------------------------------------------
@@ -85,7 +95,9 @@ __global__ void __launch_bounds__(256) star_generic(StarParams p, const Push pus
   auto xs = [&](int k) { return __fadd_rn(__ldg(u + i - k * sx), __ldg(u + i + k * sx)); };
   auto ys = [&](int k) { return __fadd_rn(__ldg(u + i - k * sy), __ldg(u + i + k * sy)); };
   auto zs = [&](int k) { return __fadd_rn(__ldg(u + i - k), __ldg(u + i + k)); };
-  const float v = star_point<0, 0, 0>(p, c0, u2v, mv, p.r[0], p.r[1], p.r[2], xs, ys, zs);
+  const float av = p.Av ? __ldg(p.Av + i) : p.A;
+  const float bv = p.Av ? (p.Bv ? __ldg(p.Bv + i) : 0.0f) : p.B;
+  const float v = star_point<0, 0, 0>(p, c0, u2v, mv, p.r[0], p.r[1], p.r[2], xs, ys, zs, av, bv);
   p.u1[i] = v;
   if (push.ndir) push_point(push, x, y, z, &v, 1);
 }
@@ -203,7 +215,7 @@ star_stream(StarParams p, int xchunk) {
         auto ys = [&](int k) { return __fadd_rn(f4get(yt_m[k - 1], j), f4get(yt_p[k - 1], j)); };
         auto zs = [&](int k) { return __fadd_rn(zw[S::OFF + j - k], zw[S::OFF + j + k]); };
         out[j] = star_point<R, R, R>(p, f4get(w[R], j), f4get(u2v, j), f4get(mv, j),
-                                     R, R, R, xs, ys, zs);
+                                     R, R, R, xs, ys, zs, p.A, p.B);
       }
       __stcs(reinterpret_cast<float4*>(p.u1 + px + col),
              make_float4(out[0], out[1], out[2], out[3]));
@@ -713,6 +725,53 @@ static int launch_tma2(const StarParams& p, cudaStream_t st, const int64_t full[
   return SDMP_OK;
 }
 
+// ---------------------------------------------------------------------------
+// variable-coefficient star on the generic TMA stream engine: fronts {u0},
+// centre {u0}, points {u2 (if B), A, B (if present), S}; same per-point order
+// as star_point + star_finish
+template <bool HAS_B>
+struct VarStarOp {
+  static constexpr int NF = 1, NC = 1, NP = HAS_B ? 4 : 2;
+  StarParams p{};
+  template <int R, class Ctx>
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx, bool m0, bool m1) const {
+    using T = typename Ctx::T;
+    const T c0 = c.xt(0, 0);
+    T lap = vcmul(p.csum0, c0);
+#pragma unroll
+    for (int k = 1; k <= R; ++k) lap = vcfma(p.c[0][k], vadd(c.xt(0, -k), c.xt(0, k)), lap);
+#pragma unroll
+    for (int k = 1; k <= R; ++k) lap = vcfma(p.c[1][k], vadd(c.ct(0, -k, 0), c.ct(0, k, 0)), lap);
+#pragma unroll
+    for (int k = 1; k <= R; ++k) lap = vcfma(p.c[2][k], vadd(c.ct(0, 0, -k), c.ct(0, 0, k)), lap);
+    const T u2v = HAS_B ? c.pt(0) : vconst<T>(0.f);
+    const T av = c.pt(HAS_B ? 1 : 0);
+    const T bv = HAS_B ? c.pt(2) : vconst<T>(0.f);
+    const T sv = c.pt(HAS_B ? 3 : 1);
+    T t = vmul(av, c0);
+    t = vfma(bv, u2v, t);
+    const T o = vfma(sv, lap, t);
+    vstore(p.u1, idx, o, m0, m1);
+    c.push_out(&o, 1, m0, m1);
+  }
+};
+
+template <int R>
+static int launch_var_engine(const StarParams& p, cudaStream_t st, const int64_t full[3],
+                             const Push& push) {
+  constexpr int TY = R <= 4 ? 16 : 8;
+  if (p.Bv) {
+    VarStarOp<true> op{};
+    op.p = p;
+    const float* arrs[6] = {p.u0, p.u0, p.u2, p.Av, p.Bv, p.m};
+    return launch_stream_op<R, TY, 2>(op, p.g, full, arrs, st, &push);
+  }
+  VarStarOp<false> op{};
+  op.p = p;
+  const float* arrs[4] = {p.u0, p.u0, p.Av, p.m};
+  return launch_stream_op<R, TY, 2>(op, p.g, full, arrs, st, &push);
+}
+
 static int launch_generic(const StarParams& p, cudaStream_t st, const Push& push) {
   const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
   SDMP_CHECK(nx <= 65535, "generic kernel: box x extent > 65535");
@@ -729,7 +788,7 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
                 int variant, const Push* push_in) {
   const Push nopush{};
   const Push& push = push_in ? *push_in : nopush;
-  StarParams p;
+  StarParams p{};
   int rc = make_geom(full, lo, hi, &p.g);
   if (rc) return rc;
   SDMP_CHECK(u0 && u1, "u0/u1 must be non-null");
@@ -800,7 +859,60 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
   return launch_generic(p, st, push);
 }
 
+int var_star_update(cudaStream_t st, const float* u0, const float* u2, const float* A,
+                    const float* B, const float* Sarr, float* u1, const int64_t full[3],
+                    const int64_t lo[3], const int64_t hi[3], const int32_t radius[3],
+                    const float* coeffs, int variant, const Push* push_in) {
+  const Push nopush{};
+  const Push& push = push_in ? *push_in : nopush;
+  StarParams p{};
+  int rc = make_geom(full, lo, hi, &p.g);
+  if (rc) return rc;
+  SDMP_CHECK(u0 && u1 && A && Sarr, "u0, u1, A and S must be non-null");
+  SDMP_CHECK(!B || u2, "u2 required with B");
+  if (box_empty(p.g)) return SDMP_OK;
+  p.u0 = u0; p.u2 = B ? u2 : nullptr; p.m = Sarr; p.u1 = u1; p.Av = A; p.Bv = B;
+  p.m_is_scale = 1;
+  p.A = 0.f; p.B = 0.f; p.C = 1.f;
+  float cs = 0.f;
+  for (int a = 0; a < 3; ++a) {
+    SDMP_CHECK(radius[a] >= 0 && radius[a] <= SDMP_MAX_RADIUS, "radius outside 0..8");
+    SDMP_CHECK(lo[a] >= radius[a] && hi[a] + radius[a] <= full[a], "box + radius exceeds FULL");
+    p.r[a] = radius[a];
+    for (int k = 0; k < SDMP_NCOEF; ++k) p.c[a][k] = (k <= radius[a]) ? coeffs[a * SDMP_NCOEF + k] : 0.f;
+    cs = cs + p.c[a][0];
+  }
+  p.csum0 = cs;
+  const int R = radius[0];
+  if ((variant & 0xff) != 1 && radius[1] == R && radius[2] == R && R >= 1) {
+    const float* arrs[6] = {u0, u1, u2 ? u2 : u0, A, B ? B : A, Sarr};
+    Geom g = p.g;
+    if (stream_fits(g, R) && tma_ok(full, arrs, 6)) {
+      switch (R) {
+        case 1: return launch_var_engine<1>(p, st, full, push);
+        case 2: return launch_var_engine<2>(p, st, full, push);
+        case 3: return launch_var_engine<3>(p, st, full, push);
+        case 4: return launch_var_engine<4>(p, st, full, push);
+        case 5: return launch_var_engine<5>(p, st, full, push);
+        case 6: return launch_var_engine<6>(p, st, full, push);
+        case 7: return launch_var_engine<7>(p, st, full, push);
+        case 8: return launch_var_engine<8>(p, st, full, push);
+      }
+    }
+  }
+  return launch_generic(p, st, push);
+}
+
 }  // namespace sdmp
+
+extern "C" int sdmp_var_star_update(void* stream, const float* u0, const float* u2,
+                                    const float* A, const float* B, const float* S, float* u1,
+                                    const int64_t full[3], const int64_t lo[3],
+                                    const int64_t hi[3], const int32_t radius[3],
+                                    const float* coeffs, int32_t variant) {
+  return sdmp::var_star_update((cudaStream_t)stream, u0, u2, A, B, S, u1, full, lo, hi, radius,
+                               coeffs, variant, nullptr);
+}
 
 extern "C" int sdmp_star_update(void* stream, const float* u0, const float* u2, const float* m,
                                 float* u1, const int64_t full[3], const int64_t lo[3],

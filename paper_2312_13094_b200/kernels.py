@@ -145,6 +145,44 @@ def acoustic_model(grid: Grid, so: int = 8, vp=None, name: str = "u") -> KernelD
     return KernelDef("acoustic", {"u": u, "m": m}, [], [eq], bytes_per_point=16, working_set=4)
 
 
+def damping_profile(n: int, nbl: int, h: float) -> np.ndarray:
+    """1D absorbing-layer profile along one axis (the paper's ABC layer,
+    PAPER.md:695): zero inside, (1.5 ln(1000) / nbl) (p - sin(2 pi p) / 2 pi) / h
+    at relative depth p into a layer of nbl points at either end."""
+    i = np.arange(n, dtype=np.float64)
+    depth = np.maximum(np.maximum(nbl - i, i - (n - 1 - nbl)), 0.0) / max(nbl, 1)
+    coeff = 1.5 * math.log(1000.0) / max(nbl, 1)
+    return coeff * (depth - np.sin(2.0 * math.pi * depth) / (2.0 * math.pi)) / h
+
+
+def damped_acoustic_model(grid: Grid, so: int = 8, nbl: int = 10, vp=None,
+                          name: str = "u") -> KernelDef:
+    """Acoustic with an absorbing boundary layer, written as the paper's
+    operator ``m*u.dt2 - u.laplace + damp*u.dt`` and solved by the reference
+    symbolics; runs as the variable-coefficient star family (24 B/pt)."""
+    import torch
+    u = TimeFunction(name=name, grid=grid, space_order=so, time_order=2)
+    m = Function(name=f"m_{name}", grid=grid, space_order=so)
+    damp = Function(name=f"damp_{name}", grid=grid, space_order=so)
+    nz = grid.shape[-1]
+    if vp is None:
+        _fill([m], lambda gx, gy, gz: (1.0 / _vp_law(gx, gy, gz, nz) ** 2,))
+    else:
+        _set_domain(m, (1.0 / vp ** 2).float())
+    profs = [torch.from_numpy(damping_profile(n, nbl, h)) for n, h in zip(grid.shape, grid.spacing)]
+    while len(profs) < 3:
+        profs.append(torch.zeros(1, dtype=torch.float64))
+
+    def law(gx, gy, gz):
+        dev = gx.device
+        return (profs[0].to(dev)[gx] + profs[1].to(dev)[gy] + profs[2].to(dev)[gz],)
+
+    _fill([damp], law)
+    eq = Eq(u.forward, solve(m * u.dt2 - u.laplace + damp * u.dt, u.forward))
+    return KernelDef("damped_acoustic", {"u": u, "m": m, "damp": damp}, [], [eq],
+                     bytes_per_point=24, working_set=6)
+
+
 def diffusion_model(grid: Grid, so: int = 2, name: str = "u") -> KernelDef:
     u = TimeFunction(name=name, grid=grid, space_order=so, time_order=1)
     eq = Eq(u.forward, solve(Eq(u.dt, u.laplace), u.forward))

@@ -130,6 +130,7 @@ class NativeOperatorPlan:
 
         # -- bound parameters ------------------------------------------------
         self.scale_bufs = []  # (out tensor, m tensor, C)
+        self.var_bufs = []    # (VarStarKernel, u Function, {"A"|"B"|"S": tensor})
         self.kparams = {}
         spacing = grid.spacing
         for k in op.kernels:
@@ -146,6 +147,20 @@ class NativeOperatorPlan:
                     self.keep.append(sbuf)
                 tab = R.coeff_table(coeffs, R.SDMP_NCOEF)
                 self.kparams[id(k)] = (list(tab.ravel()) + [A, B, C], mid, variant)
+            elif isinstance(k, CP.VarStarKernel):
+                if dt is None:
+                    raise ValueError("this operator needs dt")
+                nd = len(spacing)
+                coeffs = [[_f32(float(w) / (spacing[a] * spacing[a])) for w in k.weights[a]]
+                          if a < nd else [0.0] for a in range(3)]
+                ufn = op.fields[k.u]
+                names = ("A", "B", "S") if k.has_prev else ("A", "S")
+                bufs = {n: torch.zeros_like(ufn.storage[0]) for n in names}
+                ids = {n: self.plan.add_field([int(b.data_ptr())], ufn.full3) for n, b in bufs.items()}
+                self.keep.extend(bufs.values())
+                self.var_bufs.append((k, ufn, bufs))
+                tab = R.coeff_table(coeffs, R.SDMP_NCOEF)
+                self.kparams[id(k)] = (list(tab.ravel()), ids["A"], ids.get("B", -1), ids["S"])
             elif isinstance(k, CP.TTIKernel):
                 lap, d1, dt2 = tti_binding(k, spacing, dt)
                 fl = list(R.coeff_table(lap, R.SDMP_NCOEF).ravel()) + \
@@ -264,6 +279,14 @@ class NativeOperatorPlan:
             r = list(k.radius) + [0] * (3 - len(k.radius))
             ints = [R.ACT["STAR"], stream, fid[k.u], 0, u2, -1, mid, fid[k.u], 1] + lo + hi + r + [variant]
             return ints, fl
+        if isinstance(k, CP.VarStarKernel):
+            fl, fa, fb, fs = self.kparams[id(k)]
+            lo, hi = self._full_box(k.u, box)
+            u2 = fid[k.u] if k.has_prev else -1
+            r = list(k.radius) + [0] * (3 - len(k.radius))
+            ints = [R.ACT["VSTAR"], stream, fid[k.u], 0, u2, -1, fa, fb, fs, fid[k.u], 1] + \
+                lo + hi + r + [0]
+            return ints, fl
         if isinstance(k, CP.TTIKernel):
             (fl,) = self.kparams[id(k)]
             lo, hi = self._full_box(k.p, box)
@@ -356,6 +379,11 @@ class NativeOperatorPlan:
             if self._seen.get(id(sbuf)) != mfn._version:
                 R.bind_scale(sbuf, mfn.storage[0], C)
                 self._seen[id(sbuf)] = mfn._version
+        for k, ufn, bufs in self.var_bufs:
+            ver = tuple(self.op.fields[f]._version for f in k.statics)
+            if self._seen.get(id(k)) != ver:
+                self._bind_var(k, ufn, bufs)
+                self._seen[id(k)] = ver
         if self.static is not None:
             ver = tuple(self.op.fields[f]._version for f, _t in self.eplan.hoisted.fields)
             if self._seen.get("static") != ver:
@@ -364,6 +392,29 @@ class NativeOperatorPlan:
                 self._seen["static"] = ver
         self.plan.run(time_m, time_M)
         self.plan.sync()
+
+    def _bind_var(self, k, ufn, bufs, max_points: int = 1 << 26):
+        """A, B, S of a variable-coefficient star from its static fields:
+        evaluated in fp64 on the device (x-slabs), stored as fp32."""
+        torch = __import__("torch")
+        dom = tuple(slice(h, h + n) for h, n in zip(ufn.halo3, ufn.local3))
+        views = {f: self.op.fields[f]._domain_view(0) for f in k.statics}
+        outs = {n: b[dom] for n, b in bufs.items()}
+        nx = ufn.local3[0]
+        plane = max(1, math.prod(ufn.local3[1:]))
+        step = max(1, max_points // plane)
+        for x0 in range(0, nx, step):
+            x1 = min(nx, x0 + step)
+            vals = {f: v[x0:x1].double() for f, v in views.items()}
+            A, B, Sv = k.coefficients(vals, self.dt, self.op.grid.spacing)
+            for n, val in (("A", A), ("B", B), ("S", Sv)):
+                if n in outs:
+                    o = outs[n][x0:x1]
+                    if torch.is_tensor(val):
+                        o.copy_(val.to(o.dtype))
+                    else:
+                        o.fill_(float(val))
+        torch.cuda.synchronize()
 
     def collect_sparse(self, time_m, time_M):
         """Assemble receiver traces into ``rec.data`` on every rank."""

@@ -40,6 +40,20 @@ def acoustic(grid, tag, steps, so=8):
     return op, dt, [u], rec
 
 
+def damped(grid, tag, steps, so=8):
+    kd = KD.damped_acoustic_model(grid, so=so, nbl=5, name=f"ud{tag}")
+    u, m = kd.fields["u"], kd.fields["m"]
+    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing)))
+    ext = grid.extent
+    src = KD.point_source(grid, [tuple(0.5 * e + 0.3 for e in ext)], steps, dt, f0=0.03,
+                          name=f"srcd{tag}")
+    rc = np.stack([np.linspace(5.0, ext[0] - 5.0, 7), np.full(7, 0.5 * ext[1]),
+                   np.full(7, 0.31 * ext[2])], 1)
+    rec = SparseTimeFunction(f"recd{tag}", grid, 7, steps, coordinates=rc)
+    op = Operator([kd, src.inject(u.forward, expr=src * S.DT ** 2 / m), rec.interpolate(u)])
+    return op, dt, [u], rec
+
+
 def tti(grid, tag, steps, so=8):
     kd = KD.tti_model(grid, so=so)
     rng = np.random.default_rng(0)
@@ -78,7 +92,8 @@ def main():
     steps = int(os.environ.get("STEPS", "12"))
     failures = []
     results = {}
-    cases = [("acoustic", acoustic, {}), ("tti", tti, {}), ("elastic", elastic, {}),
+    cases = [("acoustic", acoustic, {}), ("damped", damped, {}), ("tti", tti, {}),
+             ("elastic", elastic, {}),
              ("visco", elastic, {"visco": True, "so": 16})]
     only = os.environ.get("FAMILIES")
     if only:

@@ -252,3 +252,47 @@ def test_static_field_update_between_applies():
     m2.data[...] = m2.data[...] * np.float32(0.5)
     op2.apply(time_M=steps - 1, dt=dt)
     assert np.array_equal(u1.data_gather(), u2.data_gather())
+
+
+@pytest.mark.parametrize("so", [4, 8, 16])
+def test_damped_acoustic_vs_oracle(so):
+    """Acoustic with an absorbing layer (m u.dt2 - lap u + damp u.dt, solved by
+    the reference symbolics) -> variable-coefficient star; A, B, S bound on
+    the device and the same fp32 values fed to the oracle."""
+    shape, steps = (40, 36, 44), 30
+    grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
+    kd = KD.damped_acoustic_model(grid, so=so, nbl=6, name=f"ud{so}")
+    u, m = kd.fields["u"], kd.fields["m"]
+    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing)))
+    ext = grid.extent
+    src = KD.point_source(grid, [tuple(0.5 * e + 1.3 for e in ext)], steps, dt, f0=0.030,
+                          name=f"srcd{so}")
+    rec = SparseTimeFunction(f"recd{so}", grid, 7, steps,
+                             coordinates=np.stack([np.linspace(5.0, ext[0] - 5.0, 7)] +
+                                                  [np.full(7, 0.37 * e) for e in ext[1:]], 1))
+    op = Operator([kd, src.inject(u.forward, expr=src * S.DT ** 2 / m), rec.interpolate(u)])
+    assert type(op.kernels[0]).__name__ == "VarStarKernel"
+    op.apply(time_M=steps - 1, dt=dt, mpi="full")
+    plan = next(iter(op._plans.values()))
+    _k, ufn, bufs = plan.var_bufs[0]
+    dom = tuple(slice(hh, hh + n) for hh, n in zip(ufn.halo3, ufn.local3))
+    coef = {n: b[dom].double().cpu().numpy() for n, b in bufs.items()}
+    C = float(np.float32(dt * dt))
+    h = grid.spacing
+    sp = P.SparseSpec(shape, h, src.coordinates, src.data.astype(np.float64), "u", ("m", C),
+                      rec.coordinates, "u")
+    prob = P.var_star(3, so, star_coeffs(so, h), True, sparse=sp, shape=shape, extra=("m",))
+    sim = Simulation(prob, shape)
+    for n in ("A", "B", "S"):
+        sim.write_global(n, coef[n])
+    sim.write_global("m", m.data_gather().astype(np.float64))
+    sim.run(0, steps - 1)
+    want = sim.gather("u", steps % 3)
+    got = u.data_gather()
+    err = rel_l2(got, want)
+    assert err <= REL, (err, np.abs(got - want).max())
+    terr = rel_l2(rec.data, np.array([sim.traces[t] for t in range(steps)]))
+    assert terr <= REL, terr
+    # the layer damps: the coefficient arrays differ from the undamped (2, -1) inside it
+    assert coef["A"].max() > 2.0 - 1e-6 and coef["B"].min() > -1.0 - 1e-6
+    assert np.any(coef["B"] > -0.999)
