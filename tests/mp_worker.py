@@ -40,6 +40,14 @@ def acoustic(grid, tag, steps, so=8):
     return op, dt, [u], rec
 
 
+def diffusion(grid, tag, steps, so=4):
+    kd = KD.diffusion_model(grid, so=so, name=f"ud{tag}")
+    u = kd.fields["u"]
+    u.data[...] = np.float32(np.random.default_rng(3).random(grid.shape))
+    dt = float(np.float32(0.1 * min(grid.spacing) ** 2))
+    return Operator([kd]), dt, [u], None
+
+
 def damped(grid, tag, steps, so=8):
     kd = KD.damped_acoustic_model(grid, so=so, nbl=5, name=f"ud{tag}")
     u, m = kd.fields["u"], kd.fields["m"]
@@ -92,7 +100,8 @@ def main():
     steps = int(os.environ.get("STEPS", "12"))
     failures = []
     results = {}
-    cases = [("acoustic", acoustic, {}), ("damped", damped, {}), ("tti", tti, {}),
+    cases = [("acoustic", acoustic, {}), ("diffusion", diffusion, {}), ("damped", damped, {}),
+             ("tti", tti, {}),
              ("elastic", elastic, {}),
              ("visco", elastic, {"visco": True, "so": 16})]
     only = os.environ.get("FAMILIES")
