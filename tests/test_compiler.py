@@ -175,3 +175,35 @@ def test_dump_plan_listings():
     full = CP.dump_plan([k], 4, "full", [eq])
     assert full.index("CORE") < full.index("HaloWaitList") < full.index("REMAINDER")
     assert "HaloSpot" not in CP.dump_plan([k], 1, None, [eq])
+
+
+@pytest.mark.parametrize("dims", [(4, 2, 1), (2, 2, 1), (4, 1, 1)])
+def test_full_mode_fused_push_covers_every_send_box(dims):
+    """Host logic of the fused exchange for every rank of the 8-GPU layout:
+    each message's send box lies inside the union of the OWNED slabs that push
+    it (so every halo value a neighbour reads is stored by a slab kernel), the
+    push lists fit the 8-direction limit, and CORE never intersects a send box."""
+    from paper_2312_13094_b200.distfield import diagonal_messages
+    eq, u, m = acoustic_eq(8, 3, 32)
+    k = CP.recognise([eq])[0]
+    shape = tuple(32 * d for d in dims)
+    d = DC.Decomposition.create(shape, int(np.prod(dims)), dims)
+    an = CP.halo_phases([k], d.nranks)
+    for rank in range(d.nranks):
+        p = CP.lower_mode(an, d, rank, "full")
+        posts = [a for a in p.actions if a.kind == "post"]
+        assert posts and all(a.pushed for a in posts)
+        slabs = [a for a in p.actions if a.kind == "compute" and a.region == "OWNED"]
+        core = [a for a in p.actions if a.kind == "compute" and a.region == "CORE"]
+        msgs = diagonal_messages(d, rank, k.radius)
+        assert all(a.push is not None and len(a.push[1]) <= 8 for a in slabs)
+        covered = np.zeros(d.local_shape(rank), dtype=bool)
+        for a in slabs:
+            covered[tuple(slice(lo, hi) for lo, hi in zip(*a.box))] = True
+        for msg in msgs:
+            box = tuple(slice(lo, hi) for lo, hi in zip(*msg.send))
+            assert covered[box].all(), (rank, msg)
+            for c in core:
+                inter = [max(a0, b0) < min(a1, b1) for a0, a1, b0, b1 in
+                         zip(c.box[0], c.box[1], msg.send[0], msg.send[1])]
+                assert not all(inter), (rank, msg)
