@@ -399,8 +399,13 @@ def main():
                    "transport": ("fused: OWNED-slab kernels store into peer halos (NVLink)"
                                  if fused else "copy engines (cudaMemcpy3DAsync, 4 streams)"),
                    "post_ms_rank0": post_ms,
-                   "link_gbs_rank0": sent / (post_ms * 1e-3) / 1e9 if post_ms > 0 else None,
+                   "link_gbs_rank0": (sent / (post_ms * 1e-3) / 1e9
+                                      if post_ms > 0 and not fused else None),
                    "link_peak_gbs": 900.0}
+        if fused:
+            exposed["link_note"] = ("halos are stored by the OWNED-slab kernels while they "
+                                    "compute (no separate transfer to time); post_ms_rank0 is "
+                                    "the slab kernels' time, the exposed time is the cost")
 
     # per-rank action timings (skew between ranks shows up as WAIT time)
     rank_actions = ctx.allgather([[int(r[2]), round(r[4], 4)] for r in rows]) if N > 1 else None
