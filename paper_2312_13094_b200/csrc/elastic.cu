@@ -310,24 +310,21 @@ struct ViscoOp {
 template <int R, class Op>
 static int launch_el_stream(const Op& op, const Geom& g, const int64_t full[3],
                             const float* const* arrs, cudaStream_t st, const Push& push) {
-  // velocity (few operands, many taps) is issue bound: packed pairs; the
-  // stress phases (8-15 pointwise operands) are bandwidth bound: one point
-  // per thread keeps stages small and the ring deep (measured, r01).
-#ifndef SDMP_STRESS_V
-#define SDMP_STRESS_V 1
-#endif
-#ifndef SDMP_STRESS_TYW
-#define SDMP_STRESS_TYW 8
-#endif
-  constexpr int V = Op::NP <= 4 ? 2 : SDMP_STRESS_V;
-  constexpr int TYW = Op::NP <= 4 ? 8 : SDMP_STRESS_TYW;
+  // Launch shapes measured per op and radius (r02 A/B, 512^3):
+  //  velocity (NP 4): packed pairs, 16 rows (8 beyond R = 4: registers);
+  //  elastic stress (NP 8): packed pairs, 8 rows (R = 4: 1.52 vs 1.60 ms;
+  //  R = 6: 1.64 vs 2.37 ms; R = 8: 1.86 vs 2.45 ms against one point/thread);
+  //  visco stress (NP 15): packed pairs, 16 rows up to R = 4 (3.12 vs 3.82 ms),
+  //  one point per thread and 8 rows beyond (3.09 vs 3.22 ms at R = 8).
+  constexpr bool vel = Op::NP <= 4, visco = Op::NP == 15;
+  constexpr int V = (visco && R > 4) ? 1 : 2;
+  constexpr int TYN = vel ? 16 : (visco ? 16 : 8);
   const int ny = g.hi[1] - g.lo[1];
   if constexpr (R <= 4) {
     if (ny <= 4) return launch_stream_op<R, 4, V>(op, g, full, arrs, st, &push);
-    return launch_stream_op<R, 16, V>(op, g, full, arrs, st, &push);
+    return launch_stream_op<R, TYN, V>(op, g, full, arrs, st, &push);
   } else {
-    if (ny <= 8) return launch_stream_op<R, 8, V>(op, g, full, arrs, st, &push);
-    return launch_stream_op<R, TYW, V>(op, g, full, arrs, st, &push);
+    return launch_stream_op<R, 8, V>(op, g, full, arrs, st, &push);
   }
 }
 
