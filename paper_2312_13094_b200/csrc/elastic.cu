@@ -316,15 +316,26 @@ static int launch_el_stream(const Op& op, const Geom& g, const int64_t full[3],
   //  R = 6: 1.64 vs 2.37 ms; R = 8: 1.86 vs 2.45 ms against one point/thread);
   //  visco stress (NP 15): packed pairs, 16 rows up to R = 4 (3.12 vs 3.82 ms),
   //  one point per thread and 8 rows beyond (3.09 vs 3.22 ms at R = 8).
+#ifndef SDMP_VEL_TYN
+#define SDMP_VEL_TYN 16
+#endif
+#ifndef SDMP_VEL_TYW
+#define SDMP_VEL_TYW 8
+#endif
+#ifndef SDMP_VEL_VW
+#define SDMP_VEL_VW 2
+#endif
   constexpr bool vel = Op::NP <= 4, visco = Op::NP == 15;
-  constexpr int V = (visco && R > 4) ? 1 : 2;
-  constexpr int TYN = vel ? 16 : (visco ? 16 : 8);
+  constexpr int V = (visco && R > 4) ? 1 : ((vel && R > 4) ? SDMP_VEL_VW : 2);
+  constexpr int TYN = vel ? SDMP_VEL_TYN : (visco ? 16 : 8);
+  constexpr int TYW = vel ? SDMP_VEL_TYW : 8;
   const int ny = g.hi[1] - g.lo[1];
   if constexpr (R <= 4) {
     if (ny <= 4) return launch_stream_op<R, 4, V>(op, g, full, arrs, st, &push);
     return launch_stream_op<R, TYN, V>(op, g, full, arrs, st, &push);
   } else {
-    return launch_stream_op<R, 8, V>(op, g, full, arrs, st, &push);
+    if (ny <= 8) return launch_stream_op<R, 8, V>(op, g, full, arrs, st, &push);
+    return launch_stream_op<R, TYW, V>(op, g, full, arrs, st, &push);
   }
 }
 
