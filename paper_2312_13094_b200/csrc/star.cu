@@ -759,7 +759,13 @@ struct VarStarOp {
 template <int R>
 static int launch_var_engine(const StarParams& p, cudaStream_t st, const int64_t full[3],
                              const Push& push) {
-  constexpr int TY = R <= 4 ? 16 : 8;
+#ifndef SDMP_VSTAR_TYN
+#define SDMP_VSTAR_TYN 16
+#endif
+#ifndef SDMP_VSTAR_TYW
+#define SDMP_VSTAR_TYW 8
+#endif
+  constexpr int TY = R <= 4 ? SDMP_VSTAR_TYN : SDMP_VSTAR_TYW;
   if (p.Bv) {
     VarStarOp<true> op{};
     op.p = p;

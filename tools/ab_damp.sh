@@ -1,0 +1,4 @@
+for v in "$@"; do for so in 8 16; do
+SDMP_LIB=abtest/libsdmp_$v.so python bench.py --kernel damped --so $so --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$v SO-$so', round(d['value'],1), round(d['roofline']['frac'],3))"
+done; done
