@@ -59,18 +59,10 @@ struct TMaps {
   CUtensorMap m[kMaxMaps];
 };
 
-// Op::kRing (optional, default false): unroll the x loop into a register ring
-template <class Op, class = void>
-struct RingOf {
-  static constexpr bool value = false;
-};
-template <class Op>
-struct RingOf<Op, std::void_t<decltype(Op::kRing)>> {
-#ifndef SDMP_RING
-#define SDMP_RING 1
-#endif
-  static constexpr bool value = SDMP_RING && Op::kRing;
-};
+// (r02 A/B, dropped: a register-ring x-window unrolled by 2R+1 — i-cache
+// bound for the large ops; pointwise operands loaded straight from global
+// memory one plane ahead instead of TMA-staged — latency bound, 1.3-1.6x
+// slower stress phases.)
 
 // Op::kCtas (optional, default 1): resident CTAs per SM (launch bounds and
 // the shared-memory ring are sized for it)
@@ -258,34 +250,7 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
 #pragma unroll
     for (int k = 0; k < W; ++k) w[f][k] = vconst<T>(0.f);
 
-  if constexpr (RingOf<Op>::value) {
-    // x-window as a register ring: the loop is unrolled by the window length
-    // W so every slot index is a compile-time constant (no register moves
-    // to slide the window; W x the code).  r02 A/B: no current op gains
-    // (TTI flat, visco velocity -12%), so none sets kRing.
-    for (int i0 = 0; i0 < nit; i0 += W) {
-#pragma unroll
-      for (int j = 0; j < W; ++j) {
-        const int i = i0 + j;
-        if (i < nit) {
-          const int s = i % L::S;
-          mbar_wait(&full_bar[s], (i / L::S) & 1);
-          const unsigned char* st = sm + s * L::STAGE;
-#pragma unroll
-          for (int f = 0; f < NF; ++f)
-            w[f][j] = vload<V>(reinterpret_cast<const float*>(st + f * L::FRONT) + warp * L::TZ +
-                               V * lane);
-          if (i >= 2 * R && active) {
-            const int x = xa + i - 2 * R;
-            StreamCtx<R, TY, V, NF, NC, NP> ctx{w, st, warp, lane, j, &push, x, y, z};
-            op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0, m1);
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty_bar[s]);
-        }
-      }
-    }
-  } else {
+  {
     // sliding window: newest plane at slot 2R (rotation W - 1)
     for (int i = 0; i < nit; ++i) {
       const int s = i % L::S;
