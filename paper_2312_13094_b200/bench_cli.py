@@ -198,12 +198,22 @@ def main(argv=None):
     ap.add_argument("--json", action="store_true")
     ap.add_argument("--out", default=None)
     ap.add_argument("--dump-plan", action="store_true")
+    ap.add_argument("--ranks", type=int, default=None,
+                    help="expected number of ranks (one per GPU, launched by torchrun)")
+    ap.add_argument("--transport", default="nvlink",
+                    help="halo transport: nvlink (CUDA-IPC peer stores / copy engines); the "
+                         "SPEC's inproc/socket CPU transports have no GPU counterpart")
     a = ap.parse_args(argv)
+    if a.transport != "nvlink":
+        ap.error(f"transport {a.transport!r} is not available on the GPU path (use nvlink)")
     cfg = RunConfig(kernel=a.kernel, shape=tuple(int(x) for x in a.shape.split(",")), sdo=a.so,
                     steps=a.tn, mode=a.mode, check=a.check, seed=a.seed,
                     topology=tuple(int(x) for x in a.topology.split(",")) if a.topology else None)
     from .dist import context
     ctx = context()
+    if a.ranks is not None and a.ranks != ctx.size:
+        ap.error(f"--ranks {a.ranks} but {ctx.size} rank(s) were launched "
+                 "(torchrun --nproc-per-node sets the rank count)")
     if a.dump_plan:
         _g, op, _o, _dt = _build(cfg)
         if ctx.rank == 0:

@@ -68,3 +68,10 @@ def test_cli_dump_plan(capsys):
                   "--dump-plan"])
     out = capsys.readouterr().out
     assert rc == 0 and "<Callable Kernel>" in out and "Iteration time" in out
+
+
+def test_cli_rejects_cpu_transports_and_rank_mismatch():
+    with pytest.raises(SystemExit):
+        BC.main(["--transport", "socket", "--dump-plan"])
+    with pytest.raises(SystemExit):
+        BC.main(["--ranks", "4", "--dump-plan", "--shape", "16,16,16", "--so", "4"])
