@@ -104,6 +104,15 @@ def _build(cfg: RunConfig, comm=None):
                               f0=0.03, name="src_bench" if comm is None else "src_ref")
         terms = [src.inject(u.forward, expr=src * S.DT ** 2 / m)]
         out = [u]
+    elif cfg.kernel == "damped":
+        kd = KD.damped_acoustic_model(grid, so=cfg.sdo, nbl=max(2, min(cfg.shape) // 8),
+                                      name="u_bench" if comm is None else "u_ref")
+        u, m = kd.fields["u"], kd.fields["m"]
+        dt = float(np.float32(KD.critical_dt(4.6, grid.spacing)))
+        src = KD.point_source(grid, [tuple(0.5 * e + 1.7 for e in grid.extent)], nt, dt,
+                              f0=0.03, name="src_bench" if comm is None else "src_ref")
+        terms = [src.inject(u.forward, expr=src * S.DT ** 2 / m)]
+        out = [u]
     elif cfg.kernel == "diffusion":
         kd = KD.diffusion_model(grid, so=cfg.sdo, name="u_bench" if comm is None else "u_ref")
         u = kd.fields["u"]
@@ -187,7 +196,7 @@ def to_csv(records: Sequence[MetricsRecord]) -> str:
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--kernel", default="acoustic",
-                    choices=["acoustic", "diffusion", "tti", "elastic", "visco"])
+                    choices=["acoustic", "damped", "diffusion", "tti", "elastic", "visco"])
     ap.add_argument("--shape", default="64,64,64")
     ap.add_argument("--so", type=int, default=8)
     ap.add_argument("--tn", type=int, default=20)
