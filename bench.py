@@ -306,6 +306,18 @@ def main():
     ctx.barrier()
     ms = e0.elapsed_time(e1)
     ms_max = ctx.allreduce_max(ms)
+    # two more repetitions of the same K steps (reported, not the value):
+    # run-to-run spread of the device-timed measurement
+    repeats = [ms_max / args.steps]
+    for _ in range(2):
+        ctx.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        nplan.run(t_a, t_a + args.steps - 1, stream)
+        e1.record(stream)
+        nplan.sync()
+        torch.cuda.synchronize()
+        repeats.append(ctx.allreduce_max(e0.elapsed_time(e1)) / args.steps)
     nplan.set_tracing(True)
     ctx.barrier()
     nplan.run(t_a, t_a + args.steps - 1, stream)
@@ -438,6 +450,7 @@ def main():
                          "bytes_per_point": bpp, "points_per_launch": big_pts,
                          "launch_ms": big_ms, "peak_source": peak_src},
             "gpu_launches": launches,
+            "repeat_ms_per_step": [round(r, 4) for r in repeats],
             "e2e": e2e,
             "clocks": clk,
             "halo": exposed,
