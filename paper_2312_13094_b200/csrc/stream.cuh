@@ -75,6 +75,13 @@ struct CtasOf<Op, std::void_t<decltype(Op::kCtas)>> {
   static constexpr int value = Op::kCtas;
 };
 
+// resident CTAs per SM for a launch shape: Op::kCtas only for small tiles
+// (at most 9 warps), so taller tiles keep their full register budget
+template <class Op, int TY>
+constexpr int ctas_for() {
+  return TY + 1 <= 9 ? CtasOf<Op>::value : 1;
+}
+
 template <int V> struct VType;
 template <> struct VType<1> { using T = float; };
 template <> struct VType<2> { using T = V2; };
@@ -181,11 +188,11 @@ __device__ __forceinline__ void vstore(float* p, int64_t idx, V2 v, bool m0, boo
 
 template <int R, int TY, int V, class Op>
 __global__ void __launch_bounds__(SLayout<R, TY, V, Op::NF, Op::NC, Op::NP>::THREADS,
-                                  CtasOf<Op>::value)
+                                  (ctas_for<Op, TY>()))
 stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, const int xchunk,
               const __grid_constant__ Push push) {
   constexpr int NF = Op::NF, NC = Op::NC, NP = Op::NP;
-  using L = SLayout<R, TY, V, NF, NC, NP, CtasOf<Op>::value>;
+  using L = SLayout<R, TY, V, NF, NC, NP, ctas_for<Op, TY>()>;
   using T = typename VType<V>::T;
   // __align__(1024) keeps TMA destinations aligned without integer pointer
   // arithmetic, so the consumers keep shared-space pointers (LDS)
@@ -297,7 +304,7 @@ inline int stream_chunks(int64_t tiles, int nx, int R, int ctas = 1) {
 template <int R, int TY, int V, class Op>
 int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const float* const* ptrs,
                      cudaStream_t st, const Push* push = nullptr) {
-  using L = SLayout<R, TY, V, Op::NF, Op::NC, Op::NP, CtasOf<Op>::value>;
+  using L = SLayout<R, TY, V, Op::NF, Op::NC, Op::NP, ctas_for<Op, TY>()>;
   static_assert(Op::NF + Op::NC + Op::NP <= kMaxMaps, "too many tensor maps");
   static int attr_dev = -1;
   int dev = 0;
@@ -323,7 +330,7 @@ int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const f
   }
   const int nz = g.hi[2] - g.lo[2], ny = g.hi[1] - g.lo[1], nx = g.hi[0] - g.lo[0];
   const int tz = (nz + (g.lo[2] & 3) + L::TZ - 1) / L::TZ, ty = (ny + TY - 1) / TY;
-  int nch = stream_chunks((int64_t)tz * ty, nx, R, CtasOf<Op>::value);
+  int nch = stream_chunks((int64_t)tz * ty, nx, R, ctas_for<Op, TY>());
   const int chunk = (nx + nch - 1) / nch;
   nch = (nx + chunk - 1) / chunk;
   SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");
