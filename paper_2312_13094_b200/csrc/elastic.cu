@@ -237,8 +237,12 @@ struct VelAcc {
   __device__ __forceinline__ T p() const { return c.pt(F == VX ? 0 : F == VY ? 1 : F == VZ ? 2 : 3); }
 };
 
+#ifndef SDMP_VEL_CTAS
+#define SDMP_VEL_CTAS 1
+#endif
 struct VelOp {
   static constexpr int NF = 3, NC = 5, NP = 4;
+  static constexpr int kCtas = SDMP_VEL_CTAS;
   float* out[3];
   ElCoef k;
   template <int R, class Ctx>
@@ -271,8 +275,12 @@ struct StrAcc {
   }
 };
 
+#ifndef SDMP_STRESS_CTAS
+#define SDMP_STRESS_CTAS 1
+#endif
 struct StressOp {
   static constexpr int NF = 3, NC = 3, NP = 8;
+  static constexpr int kCtas = SDMP_STRESS_CTAS;
   float* out[6];
   ElCoef k;
   template <int R, class Ctx>

@@ -729,9 +729,13 @@ static int launch_tma2(const StarParams& p, cudaStream_t st, const int64_t full[
 // variable-coefficient star on the generic TMA stream engine: fronts {u0},
 // centre {u0}, points {u2 (if B), A, B (if present), S}; same per-point order
 // as star_point + star_finish
+#ifndef SDMP_VSTAR_CTAS
+#define SDMP_VSTAR_CTAS 1
+#endif
 template <bool HAS_B>
 struct VarStarOp {
   static constexpr int NF = 1, NC = 1, NP = HAS_B ? 4 : 2;
+  static constexpr int kCtas = SDMP_VSTAR_CTAS;
   StarParams p{};
   template <int R, class Ctx>
   __device__ __forceinline__ void point(const Ctx& c, int64_t idx, bool m0, bool m1) const {
