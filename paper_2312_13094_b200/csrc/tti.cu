@@ -218,8 +218,15 @@ struct UAcc {
   __device__ __forceinline__ T q() const { return c.pt(Q); }
 };
 
+#ifndef SDMP_UOP_CTAS
+#define SDMP_UOP_CTAS 1
+#endif
+#ifndef SDMP_UOP_VN
+#define SDMP_UOP_VN 2
+#endif
 struct UOp {
   static constexpr int NF = 4, NC = 5, NP = 6;
+  static constexpr int kCtas = SDMP_UOP_CTAS;
   float* out[2];
   TTICoef k;
   template <int R, class Ctx>
@@ -254,7 +261,7 @@ static int launch_tti_stream(const Op& op, const Geom& g, const int64_t full[3],
 #ifndef SDMP_UOP_TY
 #define SDMP_UOP_TY 12
 #endif
-    constexpr int VG = upd ? 2 : SDMP_GOP_V;
+    constexpr int VG = upd ? SDMP_UOP_VN : SDMP_GOP_V;
     if (ny <= 8) return launch_stream_op<R, 8, VG>(op, g, full, arrs, st, push);
     return launch_stream_op<R, upd ? SDMP_UOP_TY : SDMP_GOP_TY, VG>(op, g, full, arrs, st, push);
   } else {
