@@ -294,8 +294,12 @@ struct StressOp {
   }
 };
 
+#ifndef SDMP_VISCO_CTAS
+#define SDMP_VISCO_CTAS 1
+#endif
 struct ViscoOp {
   static constexpr int NF = 3, NC = 3, NP = 15;
+  static constexpr int kCtas = SDMP_VISCO_CTAS;
   float* out[12];
   ElCoef k;
   template <int R, class Ctx>
