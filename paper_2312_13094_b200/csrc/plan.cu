@@ -101,9 +101,12 @@ struct sdmp_plan {
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   // copy-engine fan-out for halo posts: messages round-robin over kCopy
   // streams so several copy engines move faces/edges concurrently
-  static constexpr int kCopy = 4;
-  cudaStream_t cs[kCopy] = {nullptr, nullptr, nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_cdone[kCopy] = {nullptr, nullptr, nullptr, nullptr};
+#ifndef SDMP_COPY_STREAMS
+#define SDMP_COPY_STREAMS 4
+#endif
+  static constexpr int kCopy = SDMP_COPY_STREAMS;
+  cudaStream_t cs[kCopy] = {};
+  cudaEvent_t ev_fork = nullptr, ev_cdone[kCopy] = {};
   std::vector<Field> fields;
   std::vector<uint32_t*> flags;  // peer flag arrays
   uint32_t* local_flags = nullptr;
