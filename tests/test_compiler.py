@@ -207,3 +207,17 @@ def test_full_mode_fused_push_covers_every_send_box(dims):
                 inter = [max(a0, b0) < min(a1, b1) for a0, a1, b0, b1 in
                          zip(c.box[0], c.box[1], msg.send[0], msg.send[1])]
                 assert not all(inter), (rank, msg)
+
+
+def test_dump_plan_tti_and_staggered():
+    g = S.GridSpec((16,) * 3, (150.0,) * 3)
+    f = lambda n, to=0, so=8: S.FieldSpec(n, g, so, to)
+    tti = CP.TTIKernel(f("p", 2), f("r", 2), f("mt"), f("e"), f("d"), (f("ax"), f("ay"), f("az")), 8)
+    txt = CP.dump_plan([tti], 2, "full")
+    assert "HaloUpdateCall(ax,ay,az) once" in txt and "CORE" in txt
+    v = tuple(f(n, 1) for n in ("vx", "vy", "vz"))
+    t = tuple(f(n, 1) for n in ("txx", "tyy", "tzz", "txy", "txz", "tyz"))
+    kv = CP.StaggeredPhase("v", v, t, (f("b"),), so=8)
+    kt = CP.StaggeredPhase("t", v, t, (f("lam"), f("mu")), so=8)
+    txt = CP.dump_plan([kv, kt], 4, "diagonal")
+    assert txt.count("HaloWaitList") == 2  # tau before v, v before tau

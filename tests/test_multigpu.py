@@ -49,3 +49,24 @@ def test_four_gpus_xy_split():
     rc, rep, err = _run(4, "2,2,1", "44,40,32", "acoustic,diffusion,damped,tti,elastic,visco")
     assert rc == 0, (rep, err)
     assert all(v["equal"] for v in rep["results"].values()), rep
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
+                    reason="needs >= 4 GPUs")
+@pytest.mark.parametrize("nproc,mode", [(2, "basic"), (4, "full"), (4, "diagonal")])
+def test_listing4_2d_multi_gpu(nproc, mode):
+    """The paper's Listing 4 (2D diffusion, 4x4 grid) decomposed over 2 / 4
+    GPUs gives the printed values."""
+    env = dict(os.environ, STENCIL_DMP_MODE=mode)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", "--master-port=29518",
+           os.path.join(ROOT, "examples", "listing4_diffusion.py")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-3000:]
+    out = res.stdout
+    i = out.index("after 2 steps")
+    body = out[i:].split("\n", 1)[1]
+    vals = [float(v) for v in body.replace("[", " ").replace("]", " ").split()[:16]]
+    a, b = 0.5, -0.25
+    want = [a, b, b, a, b, a, a, b, b, a, a, b, a, b, b, a]
+    assert vals == want, out
