@@ -70,3 +70,17 @@ def test_listing4_2d_multi_gpu(nproc, mode):
     a, b = 0.5, -0.25
     want = [a, b, b, a, b, a, a, b, b, a, a, b, a, b, b, a]
     assert vals == want, out
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_halo_wait_watchdog():
+    """A neighbour that never delivers its halo ends in a NativeError after
+    SDMP_TIMEOUT_MS (device-side watchdog), not in a hang."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29519",
+           os.path.join(ROOT, "tests", "mp_watchdog.py")]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-3000:]
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    assert out[0]["outcome"] == "timeout", out
