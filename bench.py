@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--n", type=int, default=1024, help="grid points per axis per GPU")
     ap.add_argument("--nrec", type=int, default=256)
     ap.add_argument("--kernel", default="acoustic",
-                    choices=["acoustic", "damped", "tti", "elastic", "visco"])
+                    choices=["acoustic", "damped", "rotated", "tti", "elastic", "visco"])
     ap.add_argument("--shape", default=None, help="override the global shape nx,ny,nz")
     ap.add_argument("--topology", default=None,
                     help="override the rank grid px,py,pz (default 1,1,1 / 2,1,1 / 2,2,1 / 4,2,1)")
@@ -257,6 +257,11 @@ def main():
         u, m = kd.fields["u"], kd.fields["m"]
         dt = float(np.float32(KD.critical_dt(4.6, grid.spacing)))
         terms = [src.inject(u.forward, expr=src * S.DT ** 2 / m), rec.interpolate(u)]
+    elif kname == "rotated":
+        kd = KD.rotated_model(grid, so=args.so)
+        u, m = kd.fields["u"], kd.fields["m"]
+        dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.25)))
+        terms = [src.inject(u.forward, expr=src * S.DT ** 2 / m), rec.interpolate(u)]
     elif kname == "tti":
         kd = KD.tti_model(grid, so=args.so)
         p, r, m = kd.fields["p"], kd.fields["r"], kd.fields["m"]
@@ -342,6 +347,7 @@ def main():
                                  f"star_tma2<{args.so // 2}> (acoustic SO-{args.so}, TMA pipeline, "
                                  "2 rows per thread)"),
                     "damped": f"var-star stream kernel (acoustic + ABC layer, SO-{args.so})",
+                    "rotated": f"rot_g + rot_update (SPEC tti_gxx, SO-{args.so})",
                     "tti": f"tti_g + tti_update (SO-{args.so})",
                     "elastic": f"el_velocity / el_stress (SO-{args.so})",
                     "visco": f"el_velocity / visco_stress (SO-{args.so})"}[kname]

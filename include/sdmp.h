@@ -93,6 +93,14 @@ int sdmp_tti_update(void* stream, const float* const in[10], float* p1, float* r
                     int32_t radius, const float* lap_c, const float* d1_c, float dt2,
                     int32_t variant);
 
+/* Single-field rotated operator (the SPEC's tti_gxx_kernel):
+ * m u_tt = G u with G u = sum_i D_i(a_i sum_j a_j D_j u) (nested centred first
+ * derivatives), solved u1 = 2 u0 - u2 + dt2/m G u0.  in[] = {u0, u2, m, ax,
+ * ay, az}; d1_c as for sdmp_tti_update; reads u0 up to 2*radius. */
+int sdmp_rot_update(void* stream, const float* const in[6], float* u1, const int64_t full[3],
+                    const int64_t lo[3], const int64_t hi[3], int32_t radius,
+                    const float* d1_c, float dt2);
+
 /* Staggered velocity-stress elastic / viscoelastic.
  * sc: 3 * SDMP_MAX_RADIUS staggered weights / h_a (k = 1..radius).
  * v = {vx, vy, vz}; tau = {xx, yy, zz, xy, xz, yz}. */
@@ -152,7 +160,7 @@ typedef struct sdmp_plan sdmp_plan;
 
 enum {
     SDMP_ACT_STAR = 1, SDMP_ACT_TTI = 2, SDMP_ACT_EL_V = 3, SDMP_ACT_EL_T = 4,
-    SDMP_ACT_VISCO_T = 5, SDMP_ACT_INJECT = 6, SDMP_ACT_INTERP = 7, SDMP_ACT_VSTAR = 8,
+    SDMP_ACT_VISCO_T = 5, SDMP_ACT_INJECT = 6, SDMP_ACT_INTERP = 7, SDMP_ACT_VSTAR = 8, SDMP_ACT_ROT = 9,
     SDMP_ACT_POST = 10, SDMP_ACT_WAIT = 11, SDMP_ACT_RECORD = 12, SDMP_ACT_STREAMWAIT = 13,
     SDMP_ACT_PACK = 14, SDMP_ACT_UNPACK = 15
 };

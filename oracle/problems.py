@@ -141,6 +141,21 @@ def var_star(nd, so, coeffs, with_prev=True, sparse=None, shape=None, dims=None,
     return Problem(fields, halo, [Phase([("u", 0)], (r,) * nd, compute, before, after)])
 
 
+def rotated(so, d1_c, dt2, sparse=None, shape=None, dims=None):
+    """Single-field rotated operator (SPEC tti_gxx_kernel): fields u, m, a*."""
+    fields = {"u": 3, "m": 1, "ax": 1, "ay": 1, "az": 1}
+
+    def compute(rk, box, time):
+        b = lambda n, t=0: rk.buf(n, time, t)
+        K.rot_update(b("u"), b("u", -1), b("m"), (b("ax"), b("ay"), b("az")), d1_c, dt2, box,
+                     b("u", 1))
+
+    before = after = None
+    if sparse is not None:
+        before, after = _sparse_hooks(shape, dims or (1,) * 3, sparse)
+    return Problem(fields, (so,) * 3, [Phase([("u", 0)], (so,) * 3, compute, before, after)])
+
+
 def tti(so, lap_c, d1_c, dt2, sparse=None, shape=None, dims=None):
     halo = (so,) * 3
     fields = {"p": 3, "r": 3, "m": 1, "epsp": 1, "delp": 1, "ax": 1, "ay": 1, "az": 1}

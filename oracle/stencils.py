@@ -118,6 +118,24 @@ def tti_update(p0, p2, r0, r2, m, epsp, delp, dirc, lap_c, d1_c, dt2, box, p1, r
     r1[s] = 2.0 * r0[s] - r2[s] + sc * (delp[s] * h0p + gr)
 
 
+def rot_update(u0, u2, m, dirc, d1_c, dt2, box, u1):
+    """Single-field rotated operator (tti_gxx_kernel):
+    m u_tt = G u with G u = sum_i d_i(a_i sum_j a_j d_j u) (nested centred
+    first derivatives); u1 = 2 u0 - u2 + dt2/m G u0."""
+    R = len(d1_c[0]) - 1
+    gbox = grow(box, R)
+    g = np.zeros(tuple(h - l for l, h in zip(*gbox)))
+    for j in range(3):
+        g += dirc[j][_sl(gbox)] * first_derivative(u0, gbox, j, d1_c[j])
+    G = np.zeros(tuple(h - l for l, h in zip(*box)))
+    for i in range(3):
+        tmp = np.zeros(u0.shape)
+        tmp[_sl(gbox)] = dirc[i][_sl(gbox)] * g
+        G += first_derivative(tmp, box, i, d1_c[i])
+    s = _sl(box)
+    u1[s] = 2.0 * u0[s] - u2[s] + dt2 / m[s] * G
+
+
 # --- staggered first derivatives (Virieux 1986) --------------------------------
 
 def dplus(f, box, a, c):

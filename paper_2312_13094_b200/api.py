@@ -522,7 +522,8 @@ class Operator:
             if hasattr(e, "kernels"):  # KernelDef from paper_2312_13094_b200.kernels
                 kernel_like.extend(e.kernels)
                 kernel_like.extend(_as_update(q) for q in getattr(e, "equations", []))
-            elif isinstance(e, (CP.StarKernel, CP.TTIKernel, CP.StaggeredPhase)):
+            elif isinstance(e, (CP.StarKernel, CP.VarStarKernel, CP.RotatedKernel, CP.TTIKernel,
+                                CP.StaggeredPhase)):
                 kernel_like.append(e)
             else:
                 kernel_like.append(_as_update(e))

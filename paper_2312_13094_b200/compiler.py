@@ -191,6 +191,85 @@ class TTIKernel:
     bytes_per_point = 48
 
 
+@dataclass(eq=False)
+class RotatedKernel:
+    """Single-field rotated operator, the SPEC's tti_gxx_kernel
+    (SPEC.md:594-601): m u_tt = G u with G = sum_i D_i(a_i sum_j a_j D_j u)
+    (nested centred first derivatives, the reference's Deriv(a * Deriv)
+    lowering, symbolics.py:556-566), solved u1 = 2 u0 - u2 + dt^2/m G u0.
+    Recognised by exact comparison with the reference discretization."""
+
+    u: S.FieldSpec
+    m: S.FieldSpec
+    a: Tuple[S.FieldSpec, S.FieldSpec, S.FieldSpec]
+    so: int
+    family: str = "rotated"
+
+    @property
+    def radius(self):
+        return (self.so // 2,) * 3
+
+    def reads(self):
+        zero = (0, 0, 0)
+        out = [(self.u, 0, (self.so,) * 3), (self.u, -1, zero), (self.m, 0, zero)]
+        out += [(ai, 0, self.radius) for ai in self.a]
+        return out
+
+    def writes(self):
+        return [(self.u, 1)]
+
+    bytes_per_point = 28  # u0, u2, m, a_x, a_y, a_z read; u1 written
+
+
+def rotated_update(u: S.FieldSpec, m: S.FieldSpec, a) -> S.StencilEquation:
+    """The reference discretization of m u_tt = G u."""
+    inner = S.add(*(S.mul(a[j].at(), u.d(j)) for j in range(3)))
+    gxx = S.add(*(S.Deriv(S.mul(a[i].at(), inner), i, 1) for i in range(3)))
+    return S.solve_forward(S.Eq(m.at() * u.dt2 - gxx), u.forward)
+
+
+def recognise_rotated(eq: S.StencilEquation) -> Optional[RotatedKernel]:
+    """Match a solved update against rotated_update for some assignment of
+    its static fields to (m, a_x, a_y, a_z), by exact evaluation at random
+    rational bindings (or None)."""
+    u = eq.lhs.spec
+    if (u.is_static or eq.lhs.tshift != 1 or any(eq.lhs.offsets) or eq.temporaries
+            or u.grid.ndims != 3 or u.time_order != 2):
+        return None
+    accs = S.accesses(eq.rhs)
+    statics = {a.spec for a in accs if a.spec != u}
+    if len(statics) != 4 or any(not f.is_static for f in statics):
+        return None
+    pointwise = [f for f in statics if all(not any(a.offsets) for a in accs if a.spec == f)]
+    if len(pointwise) != 1:
+        return None
+    m = pointwise[0]
+    others = sorted(statics - {m}, key=lambda f: f.name)
+    leaves = sorted({S.format_expr(n) for n in _leaves(eq.rhs)})
+    rng = random.Random(99)
+    samples = [{k: Fraction(rng.randint(1, 40), rng.randint(1, 12)) for k in leaves}
+               for _ in range(2)]
+
+    def value(expr, vals):
+        bind = {}
+        for n in _leaves(expr):
+            key = S.format_expr(n)
+            if key not in vals:
+                return None
+            bind[n] = vals[key]
+        return S.eval_exact(expr, bind)
+
+    want = [value(eq.rhs, v) for v in samples]
+    import itertools
+    for perm in itertools.permutations(others):
+        exp = rotated_update(u, m, perm)
+        if {S.format_expr(n) for n in _leaves(exp.rhs)} != set(leaves):
+            continue
+        if [value(exp.rhs, v) for v in samples] == want:
+            return RotatedKernel(u, m, tuple(perm), u.space_order)
+    return None
+
+
 @dataclass
 class StaggeredPhase:
     """One phase of the staggered elastic / viscoelastic system."""
@@ -421,7 +500,7 @@ def recognise(equations: Sequence) -> List[object]:
     kernels: List[object] = []
     seen = set()
     for eq in equations:
-        if isinstance(eq, (StarKernel, VarStarKernel, TTIKernel, StaggeredPhase)):
+        if isinstance(eq, (StarKernel, VarStarKernel, RotatedKernel, TTIKernel, StaggeredPhase)):
             kernels.append(eq)
             continue
         if not isinstance(eq, S.StencilEquation):
@@ -436,9 +515,12 @@ def recognise(equations: Sequence) -> List[object]:
         if k is None:
             k = recognise_var_star(eq)
         if k is None:
+            k = recognise_rotated(eq)
+        if k is None:
             raise CompilerError(
                 "equation not recognised as a supported kernel family (acoustic, "
-                "damped acoustic, diffusion, TTI, staggered elastic/viscoelastic): "
+                "damped acoustic, diffusion, rotated G_xx, TTI, staggered "
+                "elastic/viscoelastic): "
                 + " ; ".join(S.format_equation(eq))[:300])
         kernels.append(k)
     return kernels

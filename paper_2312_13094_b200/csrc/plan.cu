@@ -36,6 +36,8 @@ int star_update(cudaStream_t, const float*, const float*, const float*, float*, 
 int var_star_update(cudaStream_t, const float*, const float*, const float*, const float*,
                     const float*, float*, const int64_t*, const int64_t*, const int64_t*,
                     const int32_t*, const float*, int, const Push*);
+int rot_update_entry(cudaStream_t, const float* const*, float*, const int64_t*, const int64_t*,
+                     const int64_t*, int32_t, const float*, float, const Push*);
 int tti_update_entry(cudaStream_t, const float* const*, float*, float*, const int64_t*,
                      const int64_t*, const int64_t*, int32_t, const float*, const float*, float,
                      const Push*);
@@ -147,6 +149,7 @@ int base_len(int kind) {
   switch (kind) {
     case SDMP_ACT_STAR: return 19;
     case SDMP_ACT_VSTAR: return 21;
+    case SDMP_ACT_ROT: return 23;
     case SDMP_ACT_TTI: return 33;
     case SDMP_ACT_EL_V: return 35;
     case SDMP_ACT_EL_T: return 43;
@@ -199,7 +202,7 @@ int launches_of(const Action& a) {
     case SDMP_ACT_STAR: case SDMP_ACT_VSTAR: case SDMP_ACT_EL_V: case SDMP_ACT_EL_T:
     case SDMP_ACT_VISCO_T: case SDMP_ACT_INJECT: case SDMP_ACT_INTERP: case SDMP_ACT_WAIT:
       return 1;
-    case SDMP_ACT_TTI:
+    case SDMP_ACT_TTI: case SDMP_ACT_ROT:
       return 2;
     case SDMP_ACT_POST:
       return 1 + (a.i[4] == 1 ? (int)a.i[3] : 0);
@@ -242,6 +245,15 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       int32_t r[3] = {(int32_t)I[17], (int32_t)I[18], (int32_t)I[19]};
       return var_star_update(st, u0, u2, A, B, Sv, u1, p->fields[I[2]].full, I + 11, I + 14, r,
                              F, (int)I[20], pp);
+    }
+    case SDMP_ACT_ROT: {
+      // [k,s, (fid,t) x {u0, u2, m, ax, ay, az}, fu1,tu1, lo3, hi3, R]
+      const float* in[6];
+      for (int k = 0; k < 6; ++k) in[k] = resolve(p, I[2 + 2 * k], I[3 + 2 * k], time);
+      float* u1 = resolve(p, I[14], I[15], time);
+      const int nc = 3 * SDMP_NCOEF;
+      return rot_update_entry(st, in, u1, p->fields[I[2]].full, I + 16, I + 19, (int32_t)I[22],
+                              F, F[nc], pp);
     }
     case SDMP_ACT_TTI: {
       const float* in[10];
@@ -594,7 +606,7 @@ static int validate(const sdmp_plan* p, const Action& a) {
   SDMP_CHECK(I[1] >= 0 && I[1] < 3, "stream id must be 0..2");
   auto fchk = [&](int64_t f) { return f >= -1 && f < (int64_t)p->fields.size(); };
   static const std::map<int, int> min_len = {
-      {SDMP_ACT_STAR, 19}, {SDMP_ACT_VSTAR, 21}, {SDMP_ACT_TTI, 33}, {SDMP_ACT_EL_V, 35}, {SDMP_ACT_EL_T, 43},
+      {SDMP_ACT_STAR, 19}, {SDMP_ACT_VSTAR, 21}, {SDMP_ACT_ROT, 23}, {SDMP_ACT_TTI, 33}, {SDMP_ACT_EL_V, 35}, {SDMP_ACT_EL_T, 43},
       {SDMP_ACT_VISCO_T, 69}, {SDMP_ACT_INJECT, 6}, {SDMP_ACT_INTERP, 5}, {SDMP_ACT_POST, 6},
       {SDMP_ACT_WAIT, 4}, {SDMP_ACT_RECORD, 3}, {SDMP_ACT_STREAMWAIT, 3}};
   auto it = min_len.find((int)I[0]);
@@ -611,6 +623,10 @@ static int validate(const sdmp_plan* p, const Action& a) {
                      fchk(I[7]) && fchk(I[8]) && I[8] >= 0 && fchk(I[9]) && I[9] >= 0,
                  "vstar: field id");
       SDMP_CHECK((int)a.f.size() >= 3 * SDMP_NCOEF, "vstar: float params");
+      break;
+    case SDMP_ACT_ROT:
+      for (int k = 0; k < 7; ++k) SDMP_CHECK(fchk(I[2 + 2 * k]) && I[2 + 2 * k] >= 0, "rot: field id");
+      SDMP_CHECK((int)a.f.size() >= 3 * SDMP_NCOEF + 1, "rot: float params");
       break;
     case SDMP_ACT_INJECT:
       SDMP_CHECK(I[5] >= 0 && I[5] < (int64_t)p->sparse.size(), "inject: set id");

@@ -112,6 +112,30 @@ __device__ __forceinline__ void u_point(const A& a, const TTICoef& c, typename A
   r1 = vfma(sc, rr, rt);
 }
 
+// ---- single-field rotated operator (the SPEC's tti_gxx_kernel):
+// m u_tt = G u,  G u = sum_i D_i (a_i g),  g = sum_j a_j D_j u  (nested first
+// derivatives, the reference symbolics' Deriv(a * Deriv) lowering); solved:
+// u1 = 2 u0 - u2 + dt^2/m G u0.  Same operation order as the TTI routines.
+template <int R, class A>
+__device__ __forceinline__ typename A::T g1_point(const A& a, const TTICoef& c) {
+  using T = typename A::T;
+  const T ax = a.template q<QAX>(), ay = a.template q<QAY>(), az = a.template q<QAZ>();
+  T g = vfma(ax, dcentral<R, 0, TP>(a, c.d1[0]), vconst<T>(0.f));
+  g = vfma(ay, dcentral<R, 1, TP>(a, c.d1[1]), g);
+  return vfma(az, dcentral<R, 2, TP>(a, c.d1[2]), g);
+}
+
+template <int R, class A>
+__device__ __forceinline__ typename A::T rot_point(const A& a, const TTICoef& c) {
+  using T = typename A::T;
+  T G = outer<R, 0, TAX, TGP>(a, c.d1[0]);
+  G = vadd(G, outer<R, 1, TAY, TGP>(a, c.d1[1]));
+  G = vadd(G, outer<R, 2, TAZ, TGP>(a, c.d1[2]));
+  const T sc = vdiv(vconst<T>(c.dt2), a.template q<QM>());
+  const T ut = vfma(vconst<T>(2.f), a.template q<QR0>(), vnegz(a.template q<QP2>()));
+  return vfma(sc, G, ut);
+}
+
 // ---- generic launch ---------------------------------------------------------
 
 struct TTIGlobalAcc {
@@ -163,6 +187,30 @@ __global__ void __launch_bounds__(256) tti_update(TTIGeneric p, const Push push)
     const float v[2] = {p1, r1};
     push_point(push, x, y, z, v, 2);
   }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) rot_g(TTIGeneric p) {
+  const int z = p.g.lo[2] + blockIdx.x * 32 + threadIdx.x;
+  const int y = p.g.lo[1] + blockIdx.y * 8 + threadIdx.y;
+  const int x = p.g.lo[0] + blockIdx.z;
+  if (z >= p.g.hi[2] || y >= p.g.hi[1]) return;
+  const int64_t i = x * p.g.sx + y * p.g.sy + z;
+  TTIGlobalAcc a{p.tap, p.pnt, i, {p.g.sx, p.g.sy, 1}};
+  p.out[0][i] = g1_point<R>(a, p.c);
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) rot_update(TTIGeneric p, const Push push) {
+  const int z = p.g.lo[2] + blockIdx.x * 32 + threadIdx.x;
+  const int y = p.g.lo[1] + blockIdx.y * 8 + threadIdx.y;
+  const int x = p.g.lo[0] + blockIdx.z;
+  if (z >= p.g.hi[2] || y >= p.g.hi[1]) return;
+  const int64_t i = x * p.g.sx + y * p.g.sy + z;
+  TTIGlobalAcc a{p.tap, p.pnt, i, {p.g.sx, p.g.sy, 1}};
+  const float v = rot_point<R>(a, p.c);
+  p.out[0][i] = v;
+  if (push.ndir) push_point(push, x, y, z, &v, 1);
 }
 
 // ---- stream operators --------------------------------------------------------
@@ -238,6 +286,59 @@ struct UOp {
     vstore(out[1], idx, r1, m0, m1);
     const typename Ctx::T o[2] = {p1, r1};
     c.push_out(o, 2, m0, m1);
+  }
+};
+
+// single-field rotated operator, pass 1: fronts {u}; centres {u};
+// points {ax, ay, az}
+template <class Ctx>
+struct RGAcc {
+  using T = typename Ctx::T;
+  const Ctx& c;
+  template <int F, int AX>
+  __device__ __forceinline__ T t(int k) const {
+    return AX == 0 ? c.xt(0, k) : AX == 1 ? c.ct(0, k, 0) : c.ct(0, 0, k);
+  }
+  template <int Q>
+  __device__ __forceinline__ T q() const { return c.pt(Q - QAX); }
+};
+
+struct RGOp {
+  static constexpr int NF = 1, NC = 1, NP = 3;
+  float* out;
+  TTICoef k;
+  template <int R, class Ctx>
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx, bool m0, bool m1) const {
+    RGAcc<Ctx> a{c};
+    vstore(out, idx, g1_point<R>(a, k), m0, m1);
+  }
+};
+
+// pass 2: fronts {ax, g}; centres {ay, az, g}; points {u0, u2, m}
+template <class Ctx>
+struct RUAcc {
+  using T = typename Ctx::T;
+  const Ctx& c;
+  template <int F, int AX>
+  __device__ __forceinline__ T t(int k) const {
+    if (AX == 0) return c.xt(F == TAX ? 0 : 1, k);
+    constexpr int ci = F == TAY ? 0 : F == TAZ ? 1 : 2;
+    return AX == 1 ? c.ct(ci, k, 0) : c.ct(ci, 0, k);
+  }
+  template <int Q>
+  __device__ __forceinline__ T q() const { return c.pt(Q == QR0 ? 0 : Q == QP2 ? 1 : 2); }
+};
+
+struct RUOp {
+  static constexpr int NF = 2, NC = 3, NP = 3;
+  float* out;
+  TTICoef k;
+  template <int R, class Ctx>
+  __device__ __forceinline__ void point(const Ctx& c, int64_t idx, bool m0, bool m1) const {
+    RUAcc<Ctx> a{c};
+    const typename Ctx::T o = rot_point<R>(a, k);
+    vstore(out, idx, o, m0, m1);
+    c.push_out(&o, 1, m0, m1);
   }
 };
 
@@ -398,6 +499,89 @@ int tti_update_entry(cudaStream_t st, const float* const in[10], float* p1, floa
   return SDMP_EUNSUPPORTED;
 }
 
+template <int R>
+static int launch_rot(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const Push& push) {
+  TTIGeneric p1 = p;
+  for (int a = 0; a < 3; ++a) {
+    p1.g.lo[a] = p.g.lo[a] - R;
+    p1.g.hi[a] = p.g.hi[a] + R;
+  }
+  p1.out[0] = const_cast<float*>(p.tap[TGP]);
+  const float* a1[5] = {p.tap[TP], p.tap[TP], p.pnt[QAX], p.pnt[QAY], p.pnt[QAZ]};
+  const float* a2[8] = {p.tap[TAX], p.tap[TGP], p.tap[TAY], p.tap[TAZ], p.tap[TGP],
+                        p.pnt[QR0], p.pnt[QP2], p.pnt[QM]};
+  const bool stream = variant_env() != 1 && stream_fits(p1.g, R) && stream_fits(p.g, R) &&
+                      tma_ok(full, a1, 5) && tma_ok(full, a2, 8);
+  if (stream) {
+    constexpr int TY = R <= 4 ? 16 : 8;
+    RGOp g{};
+    g.out = p1.out[0];
+    g.k = p.c;
+    int rc = launch_stream_op<R, TY, 2>(g, p1.g, full, a1, st);
+    if (rc) return rc;
+    RUOp u{};
+    u.out = p.out[0];
+    u.k = p.c;
+    const int ny = p.g.hi[1] - p.g.lo[1];
+    if (ny <= 8) return launch_stream_op<R, 8, 2>(u, p.g, full, a2, st, &push);
+    return launch_stream_op<R, TY, 2>(u, p.g, full, a2, st, &push);
+  }
+  dim3 b(32, 8);
+  dim3 g1((p1.g.hi[2] - p1.g.lo[2] + 31) / 32, (p1.g.hi[1] - p1.g.lo[1] + 7) / 8,
+          p1.g.hi[0] - p1.g.lo[0]);
+  rot_g<R><<<g1, b, 0, st>>>(p1);
+  SDMP_LAUNCHED();
+  dim3 g2((p.g.hi[2] - p.g.lo[2] + 31) / 32, (p.g.hi[1] - p.g.lo[1] + 7) / 8,
+          p.g.hi[0] - p.g.lo[0]);
+  rot_update<R><<<g2, b, 0, st>>>(p, push);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+int rot_update_entry(cudaStream_t st, const float* const in[6], float* u1,
+                     const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
+                     int32_t radius, const float* d1_c, float dt2, const Push* push_in) {
+  const Push nopush{};
+  const Push& push = push_in ? *push_in : nopush;
+  TTIGeneric p{};
+  int rc = make_geom(full, lo, hi, &p.g);
+  if (rc) return rc;
+  if (box_empty(p.g)) return SDMP_OK;
+  SDMP_CHECK(radius >= 1 && radius <= SDMP_MAX_RADIUS, "rotated radius (SO/2) outside 1..8");
+  for (int i = 0; i < 6; ++i) SDMP_CHECK(in[i] != nullptr, "rotated inputs must be non-null");
+  for (int a = 0; a < 3; ++a)
+    SDMP_CHECK(lo[a] >= 2 * radius && hi[a] + 2 * radius <= full[a],
+               "rotated box + 2*radius exceeds FULL (halo must be >= SO)");
+  auto sc = scratch(full[0] * full[1] * full[2]);
+  if (!sc.first) {
+    set_error("rotated: scratch allocation failed");
+    return SDMP_ECUDA;
+  }
+  // in = {u0, u2, m, ax, ay, az}
+  p.tap[TP] = in[0];
+  p.tap[TAX] = in[3]; p.tap[TAY] = in[4]; p.tap[TAZ] = in[5];
+  p.tap[TGP] = sc.first;
+  p.pnt[QR0] = in[0]; p.pnt[QP2] = in[1]; p.pnt[QM] = in[2];
+  p.pnt[QAX] = in[3]; p.pnt[QAY] = in[4]; p.pnt[QAZ] = in[5];
+  p.out[0] = u1;
+  for (int a = 0; a < 3; ++a)
+    for (int k = 0; k < SDMP_NCOEF; ++k)
+      p.c.d1[a][k] = (k >= 1 && k <= radius) ? d1_c[a * SDMP_NCOEF + k] : 0.f;
+  p.c.dt2 = dt2;
+  switch (radius) {
+    case 1: return launch_rot<1>(p, st, full, push);
+    case 2: return launch_rot<2>(p, st, full, push);
+    case 3: return launch_rot<3>(p, st, full, push);
+    case 4: return launch_rot<4>(p, st, full, push);
+    case 5: return launch_rot<5>(p, st, full, push);
+    case 6: return launch_rot<6>(p, st, full, push);
+    case 7: return launch_rot<7>(p, st, full, push);
+    case 8: return launch_rot<8>(p, st, full, push);
+  }
+  set_error("rotated: unsupported radius");
+  return SDMP_EUNSUPPORTED;
+}
+
 }  // namespace sdmp
 
 extern "C" int sdmp_tti_update(void* stream, const float* const in[10], float* p1, float* r1,
@@ -407,4 +591,11 @@ extern "C" int sdmp_tti_update(void* stream, const float* const in[10], float* p
   (void)variant;
   return sdmp::tti_update_entry((cudaStream_t)stream, in, p1, r1, full, lo, hi, radius, lap_c,
                                 d1_c, dt2, nullptr);
+}
+
+extern "C" int sdmp_rot_update(void* stream, const float* const in[6], float* u1,
+                               const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
+                               int32_t radius, const float* d1_c, float dt2) {
+  return sdmp::rot_update_entry((cudaStream_t)stream, in, u1, full, lo, hi, radius, d1_c, dt2,
+                                nullptr);
 }

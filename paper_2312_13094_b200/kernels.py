@@ -230,6 +230,35 @@ def tti_model(grid: Grid, so: int = 8, vp=None) -> KernelDef:
     return KernelDef("tti", fields, [k], bytes_per_point=48, working_set=12)
 
 
+def rotated_model(grid: Grid, so: int = 8, vp=None, name: str = "u") -> KernelDef:
+    """The SPEC's tti_gxx_kernel: one field, m u_tt = G u
+    with the rotated operator G = D^T D built from direction-cosine fields
+    (theta, phi as in the TTI model), written with the reference symbolics
+    and recognised by the compiler (28 B/pt)."""
+    import torch
+    if grid.ndims != 3:
+        raise ValueError("the rotated operator is 3D")
+    u = TimeFunction(name=name, grid=grid, space_order=so, time_order=2)
+    m = Function(name=f"m_{name}", grid=grid, space_order=so)
+    a = [Function(name=f"a{c}_{name}", grid=grid, space_order=so) for c in "xyz"]
+    nz = grid.shape[-1]
+
+    def law(gx, gy, gz):
+        th = math.radians(30.0) + math.radians(5.0) * hash_uniform(gx, gy, gz, 11).double()
+        ph = math.radians(20.0) + math.radians(5.0) * hash_uniform(gx, gy, gz, 12).double()
+        out = (torch.sin(th) * torch.cos(ph), torch.sin(th) * torch.sin(ph), torch.cos(th))
+        if vp is None:
+            out = (1.0 / _vp_law(gx, gy, gz, nz) ** 2,) + out
+        return out
+
+    _fill(([m] if vp is None else []) + a, law)
+    if vp is not None:
+        _set_domain(m, (1.0 / vp ** 2).float())
+    eq = CP.rotated_update(u.spec, m.spec, tuple(f.spec for f in a))
+    return KernelDef("rotated", {"u": u, "m": m, "ax": a[0], "ay": a[1], "az": a[2]}, [], [eq],
+                     bytes_per_point=28, working_set=7)
+
+
 # ---------------------------------------------------------------------------
 # staggered elastic / viscoelastic (PAPER.md:1045-1097)
 

@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("SDMP_LIB") or os.path.join(HERE, "libsdmp.so")  # SDM
 SDMP_MAX_RADIUS = 8
 SDMP_NCOEF = SDMP_MAX_RADIUS + 1
 
-ACT = dict(STAR=1, VSTAR=8, TTI=2, EL_V=3, EL_T=4, VISCO_T=5, INJECT=6, INTERP=7, POST=10, WAIT=11,
+ACT = dict(STAR=1, VSTAR=8, ROT=9, TTI=2, EL_V=3, EL_T=4, VISCO_T=5, INJECT=6, INTERP=7, POST=10, WAIT=11,
            RECORD=12, STREAMWAIT=13)
 
 _lib = None
@@ -47,6 +47,8 @@ def _declare(lib):
                                        C.c_float, C.c_float, C.c_float, C.c_int32]),
         "sdmp_var_star_update": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64p, i64p, i64p, i32p,
                                            f32p, C.c_int32]),
+        "sdmp_rot_update": (C.c_int, [vp, C.POINTER(vp), vp, i64p, i64p, i64p, C.c_int32, f32p,
+                                      C.c_float]),
         "sdmp_tti_update": (C.c_int, [vp, C.POINTER(vp), vp, vp, i64p, i64p, i64p, C.c_int32,
                                       f32p, f32p, C.c_float, C.c_int32]),
         "sdmp_elastic_velocity": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), vp, C.POINTER(vp),

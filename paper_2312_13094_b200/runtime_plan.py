@@ -161,6 +161,12 @@ class NativeOperatorPlan:
                 self.var_bufs.append((k, ufn, bufs))
                 tab = R.coeff_table(coeffs, R.SDMP_NCOEF)
                 self.kparams[id(k)] = (list(tab.ravel()), ids["A"], ids.get("B", -1), ids["S"])
+            elif isinstance(k, CP.RotatedKernel):
+                r = k.so // 2
+                w1 = [float(c) for c in S.fd_coefficients(1, k.so)]
+                d1 = [[0.0] + [_f32(w1[r + j] / h) for j in range(1, r + 1)] for h in spacing]
+                self.kparams[id(k)] = (list(R.coeff_table(d1, R.SDMP_NCOEF).ravel()) +
+                                       [_f32(float(dt) * float(dt))],)
             elif isinstance(k, CP.TTIKernel):
                 lap, d1, dt2 = tti_binding(k, spacing, dt)
                 fl = list(R.coeff_table(lap, R.SDMP_NCOEF).ravel()) + \
@@ -287,6 +293,15 @@ class NativeOperatorPlan:
             ints = [R.ACT["VSTAR"], stream, fid[k.u], 0, u2, -1, fa, fb, fs, fid[k.u], 1] + \
                 lo + hi + r + [0]
             return ints, fl
+        if isinstance(k, CP.RotatedKernel):
+            (fl,) = self.kparams[id(k)]
+            lo, hi = self._full_box(k.u, box)
+            refs = [(k.u, 0), (k.u, -1), (k.m, 0), (k.a[0], 0), (k.a[1], 0), (k.a[2], 0),
+                    (k.u, 1)]
+            ints = [R.ACT["ROT"], stream]
+            for f, t in refs:
+                ints += [fid[f], t]
+            return ints + lo + hi + [k.so // 2], fl
         if isinstance(k, CP.TTIKernel):
             (fl,) = self.kparams[id(k)]
             lo, hi = self._full_box(k.p, box)

@@ -62,6 +62,14 @@ def damped(grid, tag, steps, so=8):
     return op, dt, [u], rec
 
 
+def rotated(grid, tag, steps, so=8):
+    kd = KD.rotated_model(grid, so=so, name=f"ur{tag}")
+    u = kd.fields["u"]
+    u.data[:] = np.float32(np.random.default_rng(4).standard_normal(grid.shape))
+    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.2)))
+    return Operator([kd]), dt, [u], None
+
+
 def tti(grid, tag, steps, so=8):
     kd = KD.tti_model(grid, so=so)
     rng = np.random.default_rng(0)
@@ -101,7 +109,7 @@ def main():
     failures = []
     results = {}
     cases = [("acoustic", acoustic, {}), ("diffusion", diffusion, {}), ("damped", damped, {}),
-             ("tti", tti, {}),
+             ("rotated", rotated, {}), ("tti", tti, {}),
              ("elastic", elastic, {}),
              ("visco", elastic, {"visco": True, "so": 16})]
     only = os.environ.get("FAMILIES")

@@ -298,3 +298,34 @@ def test_damped_acoustic_vs_oracle(so):
     # the layer damps: the coefficient arrays differ from the undamped (2, -1) inside it
     assert coef["A"].max() > 2.0 - 1e-6 and coef["B"].min() > -1.0 - 1e-6
     assert np.any(coef["B"] > -0.999)
+
+
+@pytest.mark.parametrize("so", [4, 8, 12])
+def test_rotated_gxx_vs_oracle(so):
+    """The SPEC's tti_gxx_kernel (single-field rotated operator) through the
+    public API vs the oracle on the same fp32 fields."""
+    shape, steps = (28, 24, 32), 8
+    grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
+    kd = KD.rotated_model(grid, so=so, name=f"ur{so}")
+    u = kd.fields["u"]
+    rng = np.random.default_rng(so)
+    init = np.float32(rng.standard_normal(shape))
+    u.data[:] = init
+    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.2)))
+    op = Operator([kd])
+    assert type(op.kernels[0]).__name__ == "RotatedKernel"
+    op.apply(time_M=steps - 1, dt=dt, mpi="full")
+    h = grid.spacing
+    r = so // 2
+    w1 = [float(c) for c in S.fd_coefficients(1, so)]
+    d1 = [np.float32([0.0] + [w1[r + k] / hh for k in range(1, r + 1)]).astype(np.float64)
+          for hh in h]
+    sim = Simulation(P.rotated(so, d1, float(np.float32(dt * dt))), shape)
+    for name in ("m", "ax", "ay", "az"):
+        sim.write_global(name, kd.fields[name].data_gather().astype(np.float64))
+    sim.write_global("u", init.astype(np.float64))
+    sim.run(0, steps - 1)
+    want = sim.gather("u", steps % 3)
+    got = u.data_gather()
+    err = rel_l2(got, want)
+    assert err <= REL, (err, np.abs(got - want).max())

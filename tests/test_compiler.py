@@ -221,3 +221,24 @@ def test_dump_plan_tti_and_staggered():
     kt = CP.StaggeredPhase("t", v, t, (f("lam"), f("mu")), so=8)
     txt = CP.dump_plan([kv, kt], 4, "diagonal")
     assert txt.count("HaloWaitList") == 2  # tau before v, v before tau
+
+
+def test_recognise_rotated_gxx_golden_form():
+    """The SPEC's tti_gxx_kernel written as in tests/golden/make_golden.py
+    (m u.dt2 - sum_i D_i(a_i sum_j a_j D_j u), solved by the reference
+    symbolics) is recognised as the rotated family; a perturbed update is not."""
+    g = S.GridSpec((16,) * 3, (150.0,) * 3)
+    u = S.FieldSpec("u", g, 4, 2)
+    m = S.FieldSpec("m", g, 4, 0)
+    a = [S.FieldSpec(f"a{S.AXIS_NAMES[i]}", g, 4, 0) for i in range(3)]
+    inner = S.add(*(S.mul(a[j].at(), u.d(j)) for j in range(3)))
+    gxx = S.add(*(S.Deriv(S.mul(a[i].at(), inner), i, 1) for i in range(3)))
+    eq = S.solve_forward(S.Eq(m.at() * u.dt2 - gxx), u.forward)
+    k = CP.recognise([eq])[0]
+    assert isinstance(k, CP.RotatedKernel) and k.m == m and [f.name for f in k.a] == ["ax", "ay", "az"]
+    assert k.reads()[0] == (u, 0, (4, 4, 4))
+    # swapped direction cosines in the inner derivative: a different operator
+    bad_inner = S.add(S.mul(a[1].at(), u.d(0)), S.mul(a[0].at(), u.d(1)), S.mul(a[2].at(), u.d(2)))
+    bad = S.add(*(S.Deriv(S.mul(a[i].at(), bad_inner), i, 1) for i in range(3)))
+    with pytest.raises(CP.CompilerError):
+        CP.recognise([S.solve_forward(S.Eq(m.at() * u.dt2 - bad), u.forward)])
