@@ -43,7 +43,8 @@ def parse():
     ap.add_argument("--n", type=int, default=1024, help="grid points per axis per GPU")
     ap.add_argument("--nrec", type=int, default=256)
     ap.add_argument("--kernel", default="acoustic",
-                    choices=["acoustic", "damped", "rotated", "tti", "elastic", "visco"])
+                    choices=["acoustic", "damped", "rotated", "tti", "elastic", "elastic_col",
+                             "visco"])
     ap.add_argument("--shape", default=None, help="override the global shape nx,ny,nz")
     ap.add_argument("--topology", default=None,
                     help="override the rank grid px,py,pz (default 1,1,1 / 2,1,1 / 2,2,1 / 4,2,1)")
@@ -271,7 +272,7 @@ def main():
                  src2.inject(r.forward, expr=src2 * S.DT ** 2 / m), rec.interpolate(p)]
     else:
         kd = (KD.viscoelastic_model(grid, so=args.so) if kname == "visco"
-              else KD.elastic_model(grid, so=args.so))
+              else KD.elastic_model(grid, so=args.so, collocated=kname == "elastic_col"))
         dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.15)))
         terms = []
         for c in ("txx", "tyy", "tzz"):
@@ -350,8 +351,9 @@ def main():
                     "rotated": f"rot_g + rot_update (SPEC tti_gxx, SO-{args.so})",
                     "tti": f"tti_g + tti_update (SO-{args.so})",
                     "elastic": f"el_velocity / el_stress (SO-{args.so})",
+                    "elastic_col": f"collocated el_velocity / el_stress (SO-{args.so})",
                     "visco": f"el_velocity / visco_stress (SO-{args.so})"}[kname]
-    if kname in ("elastic", "visco"):
+    if kname in ("elastic", "elastic_col", "visco"):
         kernel_label += f" [{big_a.kernel.kind} phase]"
     bpp = big_a.kernel.bytes_per_point
     peak, peak_src = load_peaks()

@@ -113,6 +113,17 @@ int sdmp_elastic_stress(void* stream, const float* const v1[3], const float* con
                         const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
                         int32_t radius, const float* sc, float dt);
 /* params = {l2m = pi*tau_ep/tau_s, mus = mu*tau_es/tau_s, its = 1/tau_s} */
+/* The SPEC's collocated elastic_kernel: the same
+ * velocity-stress system with centred first derivatives on one grid;
+ * c1: 3 * SDMP_MAX_RADIUS central first-derivative weights / h_a (k = 1..R). */
+int sdmp_elastic_colloc_velocity(void* stream, const float* const v0[3],
+                                 const float* const tau[6], const float* b, float* const v1[3],
+                                 const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
+                                 int32_t radius, const float* c1, float dt);
+int sdmp_elastic_colloc_stress(void* stream, const float* const v1[3], const float* const t0[6],
+                               const float* lam, const float* mu, float* const t1[6],
+                               const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
+                               int32_t radius, const float* c1, float dt);
 int sdmp_visco_stress(void* stream, const float* const v1[3], const float* const s0[6],
                       const float* const r0[6], const float* const params[3],
                       float* const s1[6], float* const r1[6], const int64_t full[3],

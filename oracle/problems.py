@@ -177,7 +177,7 @@ TNAMES = ("txx", "tyy", "tzz", "txy", "txz", "tyz")
 RNAMES = ("rxx", "ryy", "rzz", "rxy", "rxz", "ryz")
 
 
-def elastic(so, sc, dt, visco=False, sparse=None, shape=None, dims=None):
+def elastic(so, sc, dt, visco=False, sparse=None, shape=None, dims=None, collocated=False):
     """Staggered velocity-stress or its single-
     relaxation viscoelastic extension.  Two phases,
     two exchanges per step: stress before v, v before stress."""
@@ -193,7 +193,7 @@ def elastic(so, sc, dt, visco=False, sparse=None, shape=None, dims=None):
     def phase_v(rk, box, time):
         b = lambda n, t=0: rk.buf(n, time, t)
         K.velocity_update([b(n) for n in VNAMES], [b(n) for n in TNAMES], b("b"), sc, dt,
-                          box, [b(n, 1) for n in VNAMES])
+                          box, [b(n, 1) for n in VNAMES], collocated)
 
     def phase_t(rk, box, time):
         b = lambda n, t=0: rk.buf(n, time, t)
@@ -204,7 +204,7 @@ def elastic(so, sc, dt, visco=False, sparse=None, shape=None, dims=None):
                                   [b(n, 1) for n in RNAMES])
         else:
             K.stress_update([b(n, 1) for n in VNAMES], [b(n) for n in TNAMES], b("lam"),
-                            b("mu"), sc, dt, box, [b(n, 1) for n in TNAMES])
+                            b("mu"), sc, dt, box, [b(n, 1) for n in TNAMES], collocated)
 
     before = after = None
     if sparse is not None:

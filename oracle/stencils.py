@@ -138,8 +138,11 @@ def rot_update(u0, u2, m, dirc, d1_c, dt2, box, u1):
 
 # --- staggered first derivatives (Virieux 1986) --------------------------------
 
-def dplus(f, box, a, c):
-    """Derivative at i+1/2: sum_k c_k (f[i+k] - f[i-k+1]); c already / h."""
+def dplus(f, box, a, c, col=False):
+    """Derivative at i+1/2: sum_k c_k (f[i+k] - f[i-k+1]); c already / h.
+    ``col``: the collocated centred derivative sum_k c_k (f[i+k] - f[i-k])."""
+    if col:
+        return first_derivative(f, box, a, [0.0] + list(c))
     nd = f.ndim
     acc = np.zeros(tuple(h - l for l, h in zip(*box)))
     for k in range(1, len(c) + 1):
@@ -147,8 +150,10 @@ def dplus(f, box, a, c):
     return acc
 
 
-def dminus(f, box, a, c):
-    """Derivative at i-1/2: sum_k c_k (f[i+k-1] - f[i-k])."""
+def dminus(f, box, a, c, col=False):
+    """Derivative at i-1/2: sum_k c_k (f[i+k-1] - f[i-k]) (``col``: centred)."""
+    if col:
+        return first_derivative(f, box, a, [0.0] + list(c))
     nd = f.ndim
     acc = np.zeros(tuple(h - l for l, h in zip(*box)))
     for k in range(1, len(c) + 1):
@@ -158,35 +163,38 @@ def dminus(f, box, a, c):
 
 # v-components (x,y,z) and stress components in the order
 # xx, yy, zz, xy, xz, yz.
-def velocity_update(v0, t0, b, sc, dt, box, v1):
+def velocity_update(v0, t0, b, sc, dt, box, v1, col=False):
     """Phase 1 of elastic/viscoelastic: v1 = v0 + dt * b * div(tau0)
     (PAPER.md:1045-1051, 1066).  ``sc[a]`` staggered weights / h_a."""
     s = _sl(box)
     txx, tyy, tzz, txy, txz, tyz = t0
-    dvx = dplus(txx, box, 0, sc[0]) + dminus(txy, box, 1, sc[1]) + dminus(txz, box, 2, sc[2])
-    dvy = dminus(txy, box, 0, sc[0]) + dplus(tyy, box, 1, sc[1]) + dminus(tyz, box, 2, sc[2])
-    dvz = dminus(txz, box, 0, sc[0]) + dminus(tyz, box, 1, sc[1]) + dplus(tzz, box, 2, sc[2])
+    dvx = (dplus(txx, box, 0, sc[0], col) + dminus(txy, box, 1, sc[1], col)
+           + dminus(txz, box, 2, sc[2], col))
+    dvy = (dminus(txy, box, 0, sc[0], col) + dplus(tyy, box, 1, sc[1], col)
+           + dminus(tyz, box, 2, sc[2], col))
+    dvz = (dminus(txz, box, 0, sc[0], col) + dminus(tyz, box, 1, sc[1], col)
+           + dplus(tzz, box, 2, sc[2], col))
     bdt = dt * b[s]
     v1[0][s] = v0[0][s] + bdt * dvx
     v1[1][s] = v0[1][s] + bdt * dvy
     v1[2][s] = v0[2][s] + bdt * dvz
 
 
-def _strains(v, box, sc):
+def _strains(v, box, sc, col=False):
     vx, vy, vz = v
-    exx = dminus(vx, box, 0, sc[0])
-    eyy = dminus(vy, box, 1, sc[1])
-    ezz = dminus(vz, box, 2, sc[2])
-    exy = dplus(vx, box, 1, sc[1]) + dplus(vy, box, 0, sc[0])
-    exz = dplus(vx, box, 2, sc[2]) + dplus(vz, box, 0, sc[0])
-    eyz = dplus(vy, box, 2, sc[2]) + dplus(vz, box, 1, sc[1])
+    exx = dminus(vx, box, 0, sc[0], col)
+    eyy = dminus(vy, box, 1, sc[1], col)
+    ezz = dminus(vz, box, 2, sc[2], col)
+    exy = dplus(vx, box, 1, sc[1], col) + dplus(vy, box, 0, sc[0], col)
+    exz = dplus(vx, box, 2, sc[2], col) + dplus(vz, box, 0, sc[0], col)
+    eyz = dplus(vy, box, 2, sc[2], col) + dplus(vz, box, 1, sc[1], col)
     return exx, eyy, ezz, exy, exz, eyz
 
 
-def stress_update(v1, t0, lam, mu, sc, dt, box, t1):
+def stress_update(v1, t0, lam, mu, sc, dt, box, t1, col=False):
     """Phase 2 elastic: tau1 = tau0 + dt (lam tr(grad v) I + mu (grad v + grad v^T))."""
     s = _sl(box)
-    exx, eyy, ezz, exy, exz, eyz = _strains(v1, box, sc)
+    exx, eyy, ezz, exy, exz, eyz = _strains(v1, box, sc, col)
     l, m = lam[s], mu[s]
     tr = exx + eyy + ezz
     t1[0][s] = t0[0][s] + dt * (l * tr + 2.0 * m * exx)

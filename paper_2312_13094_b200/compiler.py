@@ -281,6 +281,9 @@ class StaggeredPhase:
     mem: Tuple[S.FieldSpec, ...] = ()
     so: int = 8
     family: str = "staggered"
+    # the SPEC's collocated elastic_kernel: centred first
+    # derivatives on one grid instead of the paper's staggered D+/D-
+    collocated: bool = False
 
     @property
     def radius(self):

@@ -31,24 +31,39 @@ enum { TXX = 0, TYY, TZZ, TXY, TXZ, TYZ, VX, VY, VZ, PB, NV_ = 10 };
 
 // First term as an explicit fma with a zero addend so that no separately
 // rounded product ever feeds an add (identical bits for float and V2).
-template <int R, int AX, int F, class A>
+// COL = true: the SPEC's collocated grid (elastic_kernel):
+// both become the centred first derivative sum_k c_k (f[k] - f[-k]) with the
+// central first-derivative weights in c.
+template <int R, int AX, int F, bool COL = false, class A>
 __device__ __forceinline__ typename A::T dplus(const A& a, const float* c) {
   using T = typename A::T;
-  T acc = vcfma(c[0], vsub(a.template t<F, AX>(1), a.template t<F, AX>(0)), vconst<T>(0.f));
+  if constexpr (COL) {
+    T acc = vcfma(c[0], vsub(a.template t<F, AX>(1), a.template t<F, AX>(-1)), vconst<T>(0.f));
 #pragma unroll
-  for (int k = 2; k <= R; ++k)
-    acc = vcfma(c[k - 1], vsub(a.template t<F, AX>(k), a.template t<F, AX>(1 - k)), acc);
-  return acc;
+    for (int k = 2; k <= R; ++k)
+      acc = vcfma(c[k - 1], vsub(a.template t<F, AX>(k), a.template t<F, AX>(-k)), acc);
+    return acc;
+  } else {
+    T acc = vcfma(c[0], vsub(a.template t<F, AX>(1), a.template t<F, AX>(0)), vconst<T>(0.f));
+#pragma unroll
+    for (int k = 2; k <= R; ++k)
+      acc = vcfma(c[k - 1], vsub(a.template t<F, AX>(k), a.template t<F, AX>(1 - k)), acc);
+    return acc;
+  }
 }
 
-template <int R, int AX, int F, class A>
+template <int R, int AX, int F, bool COL = false, class A>
 __device__ __forceinline__ typename A::T dminus(const A& a, const float* c) {
   using T = typename A::T;
-  T acc = vcfma(c[0], vsub(a.template t<F, AX>(0), a.template t<F, AX>(-1)), vconst<T>(0.f));
+  if constexpr (COL) {
+    return dplus<R, AX, F, true>(a, c);
+  } else {
+    T acc = vcfma(c[0], vsub(a.template t<F, AX>(0), a.template t<F, AX>(-1)), vconst<T>(0.f));
 #pragma unroll
-  for (int k = 2; k <= R; ++k)
-    acc = vcfma(c[k - 1], vsub(a.template t<F, AX>(k - 1), a.template t<F, AX>(-k)), acc);
-  return acc;
+    for (int k = 2; k <= R; ++k)
+      acc = vcfma(c[k - 1], vsub(a.template t<F, AX>(k - 1), a.template t<F, AX>(-k)), acc);
+    return acc;
+  }
 }
 
 // ---- per-point routines (shared by both launch shapes) --------------------
@@ -56,49 +71,49 @@ __device__ __forceinline__ typename A::T dminus(const A& a, const float* c) {
 // one velocity component: v_C += b dt (Dx + Dy + Dz) with the staggering
 // of component C (x: D+ txx, D- txy, D- txz; y: D- txy, D+ tyy, D- tyz;
 // z: D- txz, D- tyz, D+ tzz)
-template <int R, int C, class A>
+template <int R, int C, bool COL = false, class A>
 __device__ __forceinline__ typename A::T vel_comp(const A& a, const ElCoef& k) {
   using T = typename A::T;
   const T bdt = vcmul(k.dt, a.template p<PB>());
   T d;
   if constexpr (C == 0)
-    d = vadd(vadd(dplus<R, 0, TXX>(a, k.c[0]), dminus<R, 1, TXY>(a, k.c[1])),
-             dminus<R, 2, TXZ>(a, k.c[2]));
+    d = vadd(vadd(dplus<R, 0, TXX, COL>(a, k.c[0]), dminus<R, 1, TXY, COL>(a, k.c[1])),
+             dminus<R, 2, TXZ, COL>(a, k.c[2]));
   else if constexpr (C == 1)
-    d = vadd(vadd(dminus<R, 0, TXY>(a, k.c[0]), dplus<R, 1, TYY>(a, k.c[1])),
-             dminus<R, 2, TYZ>(a, k.c[2]));
+    d = vadd(vadd(dminus<R, 0, TXY, COL>(a, k.c[0]), dplus<R, 1, TYY, COL>(a, k.c[1])),
+             dminus<R, 2, TYZ, COL>(a, k.c[2]));
   else
-    d = vadd(vadd(dminus<R, 0, TXZ>(a, k.c[0]), dminus<R, 1, TYZ>(a, k.c[1])),
-             dplus<R, 2, TZZ>(a, k.c[2]));
+    d = vadd(vadd(dminus<R, 0, TXZ, COL>(a, k.c[0]), dminus<R, 1, TYZ, COL>(a, k.c[1])),
+             dplus<R, 2, TZZ, COL>(a, k.c[2]));
   return vfma(bdt, d, a.template p<VX + C>());
 }
 
-template <int R, class A>
+template <int R, bool COL = false, class A>
 __device__ __forceinline__ void vel_point(const A& a, const ElCoef& k, typename A::T out[3]) {
-  out[0] = vel_comp<R, 0>(a, k);
-  out[1] = vel_comp<R, 1>(a, k);
-  out[2] = vel_comp<R, 2>(a, k);
+  out[0] = vel_comp<R, 0, COL>(a, k);
+  out[1] = vel_comp<R, 1, COL>(a, k);
+  out[2] = vel_comp<R, 2, COL>(a, k);
 }
 
 // strains from v (logical VX, VY, VZ): exx, eyy, ezz, exy, exz, eyz
-template <int R, class A>
+template <int R, bool COL = false, class A>
 __device__ __forceinline__ void strain_point(const A& a, const ElCoef& k, typename A::T e[6]) {
-  e[0] = dminus<R, 0, VX>(a, k.c[0]);
-  e[1] = dminus<R, 1, VY>(a, k.c[1]);
-  e[2] = dminus<R, 2, VZ>(a, k.c[2]);
-  e[3] = vadd(dplus<R, 1, VX>(a, k.c[1]), dplus<R, 0, VY>(a, k.c[0]));
-  e[4] = vadd(dplus<R, 2, VX>(a, k.c[2]), dplus<R, 0, VZ>(a, k.c[0]));
-  e[5] = vadd(dplus<R, 2, VY>(a, k.c[2]), dplus<R, 1, VZ>(a, k.c[1]));
+  e[0] = dminus<R, 0, VX, COL>(a, k.c[0]);
+  e[1] = dminus<R, 1, VY, COL>(a, k.c[1]);
+  e[2] = dminus<R, 2, VZ, COL>(a, k.c[2]);
+  e[3] = vadd(dplus<R, 1, VX, COL>(a, k.c[1]), dplus<R, 0, VY, COL>(a, k.c[0]));
+  e[4] = vadd(dplus<R, 2, VX, COL>(a, k.c[2]), dplus<R, 0, VZ, COL>(a, k.c[0]));
+  e[5] = vadd(dplus<R, 2, VY, COL>(a, k.c[2]), dplus<R, 1, VZ, COL>(a, k.c[1]));
 }
 
 // logical pointwise ids of the stress phases
 enum { S0 = 0, LAM = 6, MU = 7, R0 = 8, L2M = 14, MUS = 15, ITS = 16 };
 
-template <int R, class A>
+template <int R, bool COL = false, class A>
 __device__ __forceinline__ void stress_point(const A& a, const ElCoef& k, typename A::T out[6]) {
   using T = typename A::T;
   T e[6];
-  strain_point<R>(a, k, e);
+  strain_point<R, COL>(a, k, e);
   const T l = a.template q<LAM>(), mu = a.template q<MU>();
   const T tr = vadd(vadd(e[0], e[1]), e[2]);
   const T ltr = vmul(l, tr), m2 = vcmul(2.f, mu);
@@ -185,22 +200,22 @@ struct ElGeneric {
   const int64_t i = x * p.g.sx + y * p.g.sy + z;                               \
   GlobalAcc a{p.tap, p.pnt, i, {p.g.sx, p.g.sy, 1}};
 
-template <int R>
+template <int R, bool COL = false>
 __global__ void __launch_bounds__(256) el_velocity(ElGeneric p, const Push push) {
   EL_INDEX
   float o[3];
-  vel_point<R>(a, p.k, o);
+  vel_point<R, COL>(a, p.k, o);
   p.out[0][i] = o[0];
   p.out[1][i] = o[1];
   p.out[2][i] = o[2];
   if (push.ndir) push_point(push, x, y, z, o, 3);
 }
 
-template <int R>
+template <int R, bool COL = false>
 __global__ void __launch_bounds__(256) el_stress(ElGeneric p, const Push push) {
   EL_INDEX
   float o[6];
-  stress_point<R>(a, p.k, o);
+  stress_point<R, COL>(a, p.k, o);
 #pragma unroll
   for (int c = 0; c < 6; ++c) p.out[c][i] = o[c];
   if (push.ndir) push_point(push, x, y, z, o, 6);
@@ -240,7 +255,8 @@ struct VelAcc {
 #ifndef SDMP_VEL_CTAS
 #define SDMP_VEL_CTAS 1
 #endif
-struct VelOp {
+template <bool COL = false>
+struct VelOpT {
   static constexpr int NF = 3, NC = 5, NP = 4;
   static constexpr int kCtas = SDMP_VEL_CTAS;
   float* out[3];
@@ -249,7 +265,7 @@ struct VelOp {
   __device__ __forceinline__ void point(const Ctx& c, int64_t idx, bool m0, bool m1) const {
     VelAcc<Ctx> a{c};
     typename Ctx::T o[3];
-    vel_point<R>(a, k, o);
+    vel_point<R, COL>(a, k, o);
 #pragma unroll
     for (int q = 0; q < 3; ++q) vstore(out[q], idx, o[q], m0, m1);
     c.push_out(o, 3, m0, m1);
@@ -278,7 +294,8 @@ struct StrAcc {
 #ifndef SDMP_STRESS_CTAS
 #define SDMP_STRESS_CTAS 1
 #endif
-struct StressOp {
+template <bool COL = false>
+struct StressOpT {
   static constexpr int NF = 3, NC = 3, NP = 8;
   static constexpr int kCtas = SDMP_STRESS_CTAS;
   float* out[6];
@@ -287,7 +304,7 @@ struct StressOp {
   __device__ __forceinline__ void point(const Ctx& c, int64_t idx, bool m0, bool m1) const {
     StrAcc<Ctx, NP> a{c};
     typename Ctx::T o[6];
-    stress_point<R>(a, k, o);
+    stress_point<R, COL>(a, k, o);
 #pragma unroll
     for (int q = 0; q < 6; ++q) vstore(out[q], idx, o[q], m0, m1);
     c.push_out(o, 6, m0, m1);
@@ -401,7 +418,7 @@ int elastic_velocity_impl(void* stream, const float* const v0[3],
                                      const float* const tau[6], const float* b,
                                      float* const v1[3], const int64_t full[3],
                                      const int64_t lo[3], const int64_t hi[3], int32_t radius,
-                                     const float* sc, float dt, const Push* push_in) {
+                                     const float* sc, float dt, const Push* push_in, bool colloc) {
   const Push nopush{};
   const Push& push = push_in ? *push_in : nopush;
   ElGeneric p{};
@@ -416,10 +433,19 @@ int elastic_velocity_impl(void* stream, const float* const v0[3],
   const float* arrs[12] = {tau[0], tau[3], tau[4], tau[1], tau[2], tau[3], tau[4], tau[5],
                            v0[0], v0[1], v0[2], b};
   if (variant_env() != 1 && stream_fits(p.g, radius) && tma_ok(full, arrs, 12)) {
-    VelOp op{};
+    if (colloc) {
+      VelOpT<true> op{};
+      for (int c = 0; c < 3; ++c) op.out[c] = v1[c];
+      op.k = p.k;
+      RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st, push))
+    }
+    VelOpT<false> op{};
     for (int c = 0; c < 3; ++c) op.out[c] = v1[c];
     op.k = p.k;
     RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st, push))
+  }
+  if (colloc) {
+    RADIUS_SWITCH((launch_generic(p.g, el_velocity<RR, true>, p, st, push)))
   }
   RADIUS_SWITCH(launch_generic(p.g, el_velocity<RR>, p, st, push))
 }
@@ -428,7 +454,7 @@ int elastic_stress_impl(void* stream, const float* const v1[3],
                                    const float* const t0[6], const float* lam, const float* mu,
                                    float* const t1[6], const int64_t full[3],
                                    const int64_t lo[3], const int64_t hi[3], int32_t radius,
-                                   const float* sc, float dt, const Push* push_in) {
+                                   const float* sc, float dt, const Push* push_in, bool colloc) {
   const Push nopush{};
   const Push& push = push_in ? *push_in : nopush;
   ElGeneric p{};
@@ -444,10 +470,19 @@ int elastic_stress_impl(void* stream, const float* const v1[3],
   const float* arrs[14] = {v1[0], v1[1], v1[2], v1[0], v1[1], v1[2],
                            t0[0], t0[1], t0[2], t0[3], t0[4], t0[5], lam, mu};
   if (variant_env() != 1 && stream_fits(p.g, radius) && tma_ok(full, arrs, 14)) {
-    StressOp op{};
+    if (colloc) {
+      StressOpT<true> op{};
+      for (int c = 0; c < 6; ++c) op.out[c] = t1[c];
+      op.k = p.k;
+      RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st, push))
+    }
+    StressOpT<false> op{};
     for (int c = 0; c < 6; ++c) op.out[c] = t1[c];
     op.k = p.k;
     RADIUS_SWITCH(launch_el_stream<RR>(op, p.g, full, arrs, st, push))
+  }
+  if (colloc) {
+    RADIUS_SWITCH((launch_generic(p.g, el_stress<RR, true>, p, st, push)))
   }
   RADIUS_SWITCH(launch_generic(p.g, el_stress<RR>, p, st, push))
 }
@@ -496,7 +531,8 @@ extern "C" int sdmp_elastic_velocity(void* stream, const float* const v0[3],
                                      float* const v1[3], const int64_t full[3],
                                      const int64_t lo[3], const int64_t hi[3], int32_t radius,
                                      const float* sc, float dt) {
-  return elastic_velocity_impl(stream, v0, tau, b, v1, full, lo, hi, radius, sc, dt, nullptr);
+  return elastic_velocity_impl(stream, v0, tau, b, v1, full, lo, hi, radius, sc, dt, nullptr,
+                               false);
 }
 
 extern "C" int sdmp_elastic_stress(void* stream, const float* const v1[3],
@@ -504,7 +540,8 @@ extern "C" int sdmp_elastic_stress(void* stream, const float* const v1[3],
                                    float* const t1[6], const int64_t full[3],
                                    const int64_t lo[3], const int64_t hi[3], int32_t radius,
                                    const float* sc, float dt) {
-  return elastic_stress_impl(stream, v1, t0, lam, mu, t1, full, lo, hi, radius, sc, dt, nullptr);
+  return elastic_stress_impl(stream, v1, t0, lam, mu, t1, full, lo, hi, radius, sc, dt, nullptr,
+                             false);
 }
 
 extern "C" int sdmp_visco_stress(void* stream, const float* const v1[3],
@@ -515,4 +552,23 @@ extern "C" int sdmp_visco_stress(void* stream, const float* const v1[3],
                                  float dt) {
   return visco_stress_impl(stream, v1, s0, r0, prm, s1, r1, full, lo, hi, radius, sc, dt,
                            nullptr);
+}
+
+extern "C" int sdmp_elastic_colloc_velocity(void* stream, const float* const v0[3],
+                                            const float* const tau[6], const float* b,
+                                            float* const v1[3], const int64_t full[3],
+                                            const int64_t lo[3], const int64_t hi[3],
+                                            int32_t radius, const float* c1, float dt) {
+  return elastic_velocity_impl(stream, v0, tau, b, v1, full, lo, hi, radius, c1, dt, nullptr,
+                               true);
+}
+
+extern "C" int sdmp_elastic_colloc_stress(void* stream, const float* const v1[3],
+                                          const float* const t0[6], const float* lam,
+                                          const float* mu, float* const t1[6],
+                                          const int64_t full[3], const int64_t lo[3],
+                                          const int64_t hi[3], int32_t radius, const float* c1,
+                                          float dt) {
+  return elastic_stress_impl(stream, v1, t0, lam, mu, t1, full, lo, hi, radius, c1, dt, nullptr,
+                             true);
 }

@@ -46,10 +46,10 @@ int inject(cudaStream_t, float*, const int64_t*, const int32_t*, int, const int3
            const Push*);
 int elastic_velocity_impl(void*, const float* const[3], const float* const[6], const float*,
                           float* const[3], const int64_t[3], const int64_t[3], const int64_t[3],
-                          int32_t, const float*, float, const Push*);
+                          int32_t, const float*, float, const Push*, bool);
 int elastic_stress_impl(void*, const float* const[3], const float* const[6], const float*,
                         const float*, float* const[6], const int64_t[3], const int64_t[3],
-                        const int64_t[3], int32_t, const float*, float, const Push*);
+                        const int64_t[3], int32_t, const float*, float, const Push*, bool);
 int visco_stress_impl(void*, const float* const[3], const float* const[6],
                       const float* const[6], const float* const[3], float* const[6],
                       float* const[6], const int64_t[3], const int64_t[3], const int64_t[3],
@@ -274,8 +274,10 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       for (int k = 0; k < 3; ++k) v1[k] = resolve(p, I[22 + 2 * k], I[23 + 2 * k], time);
       const int64_t* lo = I + 28;
       const int64_t* hi = I + 31;
+      // radius | collocated << 8 (the SPEC's collocated elastic_kernel)
       return elastic_velocity_impl(st, v0, tau, b, v1, p->fields[I[2]].full, lo, hi,
-                                   (int32_t)I[34], F, F[3 * SDMP_MAX_RADIUS], pp);
+                                   (int32_t)(I[34] & 0xff), F, F[3 * SDMP_MAX_RADIUS], pp,
+                                   (I[34] >> 8) & 1);
     }
     case SDMP_ACT_EL_T: {
       const float* v1[3]; const float* t0[6]; float* t1[6];
@@ -287,7 +289,8 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       const int64_t* lo = I + 36;
       const int64_t* hi = I + 39;
       return elastic_stress_impl(st, v1, t0, lam, mu, t1, p->fields[I[2]].full, lo, hi,
-                                 (int32_t)I[42], F, F[3 * SDMP_MAX_RADIUS], pp);
+                                 (int32_t)(I[42] & 0xff), F, F[3 * SDMP_MAX_RADIUS], pp,
+                                 (I[42] >> 8) & 1);
     }
     case SDMP_ACT_VISCO_T: {
       const float* v1[3]; const float* s0[6]; const float* r0[6]; const float* prm[3];

@@ -276,7 +276,10 @@ def _elastic_materials(gx, gy, gz, nz):
     return vp, vs, rho
 
 
-def elastic_model(grid: Grid, so: int = 8) -> KernelDef:
+def elastic_model(grid: Grid, so: int = 8, collocated: bool = False) -> KernelDef:
+    """Velocity-stress elastic: the paper's staggered (Virieux) grid, or with
+    ``collocated=True`` the SPEC's elastic_kernel (centred
+    first derivatives on one grid)."""
     if grid.ndims != 3:
         raise ValueError("elastic is 3D")
     v = [TimeFunction(name=n, grid=grid, space_order=so, time_order=1) for n in VNAMES]
@@ -292,12 +295,13 @@ def elastic_model(grid: Grid, so: int = 8) -> KernelDef:
 
     _fill([b, lam, mu], law)
     kv = CP.StaggeredPhase("v", tuple(f.spec for f in v), tuple(f.spec for f in t),
-                           (b.spec,), so=so)
+                           (b.spec,), so=so, collocated=collocated)
     kt = CP.StaggeredPhase("t", tuple(f.spec for f in v), tuple(f.spec for f in t),
-                           (lam.spec, mu.spec), so=so)
+                           (lam.spec, mu.spec), so=so, collocated=collocated)
     fields = {f.name: f for f in v + t}
     fields.update({"b": b, "lam": lam, "mu": mu})
-    return KernelDef("elastic", fields, [kv, kt], bytes_per_point=120, working_set=21)
+    return KernelDef("elastic_collocated" if collocated else "elastic", fields, [kv, kt],
+                     bytes_per_point=120, working_set=21)
 
 
 def viscoelastic_model(grid: Grid, so: int = 16, qp: float = 100.0, qs: float = 50.0,

@@ -54,7 +54,12 @@ def tti_binding(k: CP.TTIKernel, spacing, dt):
 
 
 def staggered_binding(k: CP.StaggeredPhase, spacing, dt):
-    c = [float(x) for x in S.staggered_coefficients(k.so)]
+    if k.collocated:  # centred first-derivative weights w_k, k = 1..R
+        r = k.so // 2
+        w1 = [float(x) for x in S.fd_coefficients(1, k.so)]
+        c = [w1[r + j] for j in range(1, r + 1)]
+    else:
+        c = [float(x) for x in S.staggered_coefficients(k.so)]
     return [[_f32(ci / h) for ci in c] for h in spacing], _f32(dt)
 
 
@@ -329,7 +334,8 @@ class NativeOperatorPlan:
             ints = [kind, stream]
             for f, t in refs:
                 ints += [fid[f], t]
-            return ints + lo + hi + [k.so // 2], fl
+            # radius | collocated << 8
+            return ints + lo + hi + [k.so // 2 | (256 if k.collocated else 0)], fl
         raise CP.CompilerError(f"no native encoding for {type(k).__name__}")
 
     def _encode_static(self, ep, decomp, rank):

@@ -80,8 +80,9 @@ def tti(grid, tag, steps, so=8):
     return Operator([kd]), dt, [kd.fields["p"], kd.fields["r"]], None
 
 
-def elastic(grid, tag, steps, so=8, visco=False):
-    kd = KD.viscoelastic_model(grid, so=so) if visco else KD.elastic_model(grid, so=so)
+def elastic(grid, tag, steps, so=8, visco=False, collocated=False):
+    kd = (KD.viscoelastic_model(grid, so=so) if visco
+          else KD.elastic_model(grid, so=so, collocated=collocated))
     rng = np.random.default_rng(1)
     t0 = np.float32(rng.standard_normal(grid.shape))
     kd.fields["txx"].data[:] = t0
@@ -110,7 +111,7 @@ def main():
     results = {}
     cases = [("acoustic", acoustic, {}), ("diffusion", diffusion, {}), ("damped", damped, {}),
              ("rotated", rotated, {}), ("tti", tti, {}),
-             ("elastic", elastic, {}),
+             ("elastic", elastic, {}), ("elastic_col", elastic, {"collocated": True}),
              ("visco", elastic, {"visco": True, "so": 16})]
     only = os.environ.get("FAMILIES")
     if only:

@@ -329,3 +329,33 @@ def test_rotated_gxx_vs_oracle(so):
     got = u.data_gather()
     err = rel_l2(got, want)
     assert err <= REL, (err, np.abs(got - want).max())
+
+
+@pytest.mark.parametrize("so", [4, 8, 16])
+def test_collocated_elastic_vs_oracle(so):
+    """The SPEC's collocated elastic_kernel vs the oracle."""
+    shape, steps = (24, 28, 20), 8
+    grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
+    kd = KD.elastic_model(grid, so=so, collocated=True)
+    rng = np.random.default_rng(2)
+    t0 = np.float32(rng.standard_normal(shape))
+    kd.fields["txx"].data[:] = t0
+    kd.fields["tyz"].data[:] = 0.5 * t0
+    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.1)))
+    Operator([kd]).apply(time_M=steps - 1, dt=dt, mpi="full")
+    r = so // 2
+    w1 = [float(c) for c in S.fd_coefficients(1, so)]
+    sc = [np.float32([w1[r + k] / hh for k in range(1, r + 1)]).astype(np.float64)
+          for hh in grid.spacing]
+    sim = Simulation(P.elastic(so, sc, float(np.float32(dt)), collocated=True), shape)
+    for name in ("b", "lam", "mu"):
+        sim.write_global(name, kd.fields[name].data_gather().astype(np.float64))
+    sim.write_global("txx", t0.astype(np.float64))
+    sim.write_global("tyz", 0.5 * t0.astype(np.float64))
+    sim.run(0, steps - 1)
+    for name in P.VNAMES + P.TNAMES:
+        want = sim.gather(name, steps % 2)
+        got = kd.fields[name].data_gather()
+        err = rel_l2(got, want)
+        assert err <= REL, (name, err, np.abs(got - want).max())
+    assert np.abs(sim.gather("vx", steps % 2)).max() > 0

@@ -29,7 +29,7 @@ def _run(nproc, topo, shape, families, steps=10, timeout=900):
                     reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("topo,shape", [("2,1,1", "40,36,32"), ("1,2,1", "36,40,32")])
 def test_two_gpus_all_families(topo, shape):
-    rc, rep, err = _run(2, topo, shape, "acoustic,diffusion,damped,rotated,tti,elastic,visco")
+    rc, rep, err = _run(2, topo, shape, "acoustic,diffusion,damped,rotated,tti,elastic,elastic_col,visco")
     assert rc == 0, (rep, err)
     assert rep["results"] and all(v["equal"] for v in rep["results"].values()), rep
 
@@ -38,7 +38,7 @@ def test_two_gpus_all_families(topo, shape):
                     reason="needs >= 4 GPUs")
 def test_four_gpus_x_interior_ranks():
     # (4,1,1): interior ranks with both x neighbours, as in the 8-GPU (4,2,1) layout
-    rc, rep, err = _run(4, "4,1,1", "64,36,32", "acoustic,diffusion,damped,rotated,tti,elastic,visco")
+    rc, rep, err = _run(4, "4,1,1", "64,36,32", "acoustic,diffusion,damped,rotated,tti,elastic,elastic_col,visco")
     assert rc == 0, (rep, err)
     assert all(v["equal"] for v in rep["results"].values()), rep
 
@@ -46,7 +46,7 @@ def test_four_gpus_x_interior_ranks():
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
                     reason="needs >= 4 GPUs")
 def test_four_gpus_xy_split():
-    rc, rep, err = _run(4, "2,2,1", "44,40,32", "acoustic,diffusion,damped,rotated,tti,elastic,visco")
+    rc, rep, err = _run(4, "2,2,1", "44,40,32", "acoustic,diffusion,damped,rotated,tti,elastic,elastic_col,visco")
     assert rc == 0, (rep, err)
     assert all(v["equal"] for v in rep["results"].values()), rep
 
