@@ -56,6 +56,12 @@ def _declare(lib):
         "sdmp_elastic_stress": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), vp, vp,
                                           C.POINTER(vp), i64p, i64p, i64p, C.c_int32, f32p,
                                           C.c_float]),
+        "sdmp_elastic_colloc_velocity": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), vp,
+                                                   C.POINTER(vp), i64p, i64p, i64p, C.c_int32,
+                                                   f32p, C.c_float]),
+        "sdmp_elastic_colloc_stress": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), vp, vp,
+                                                 C.POINTER(vp), i64p, i64p, i64p, C.c_int32,
+                                                 f32p, C.c_float]),
         "sdmp_visco_stress": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                         C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), i64p, i64p,
                                         i64p, C.c_int32, f32p, C.c_float]),

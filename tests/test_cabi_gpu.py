@@ -199,3 +199,69 @@ def test_inject_interpolate_entry_points():
     got = out.cpu().numpy()
     assert abs(got[0] - (0.3 * sf[5] + 0.7 * sf[6])) < 1e-5
     assert abs(got[1] - (0.9 * sf[400] + 0.1 * sf[401])) < 1e-5
+
+
+@pytest.mark.parametrize("so", [4, 8])
+def test_collocated_elastic_entry_points(so):
+    r = so // 2
+    full = (16 + 2 * so, 18 + 2 * so, 24 + 2 * so)
+    lo, hi = (so,) * 3, tuple(n - so for n in full)
+    rng = np.random.default_rng(so + 7)
+    rnd = lambda: np.float32(rng.standard_normal(full))
+    v0, t0 = [rnd() for _ in range(3)], [rnd() for _ in range(6)]
+    b = np.float32(0.5 + rng.random(full))
+    lam, mu = np.float32(1.0 + rng.random(full)), np.float32(0.5 + rng.random(full))
+    h, dt = 10.0, float(np.float32(0.4))
+    w1 = [float(c) for c in S.fd_coefficients(1, so)]
+    c1 = [np.float32([w1[r + k] / h for k in range(1, r + 1)]) for _ in range(3)]
+    c1t = R.coeff_table(c1, MR).ctypes.data_as(C.POINTER(C.c_float))
+    f64 = lambda x: x.astype(np.float64)
+    box, s = (lo, hi), tuple(slice(x, y) for x, y in zip(lo, hi))
+    geo = (arr(C.c_int64, full), arr(C.c_int64, lo), arr(C.c_int64, hi), r)
+    dv0, dt0, db = [dev(x) for x in v0], [dev(x) for x in t0], dev(b)
+    dv1 = [torch.zeros_like(db) for _ in range(3)]
+    call("sdmp_elastic_colloc_velocity", None, ptrs(dv0), ptrs(dt0), C.c_void_p(db.data_ptr()),
+         ptrs(dv1), *geo, c1t, C.c_float(dt))
+    wv = [np.zeros(full) for _ in range(3)]
+    K.velocity_update([f64(x) for x in v0], [f64(x) for x in t0], f64(b), [f64(c) for c in c1],
+                      dt, box, wv, col=True)
+    for g, w in zip(dv1, wv):
+        assert rel_l2(g.cpu().numpy()[s], w[s]) <= REL
+    v1 = [np.float32(w) for w in wv]
+    dv1 = [dev(x) for x in v1]
+    dlam, dmu = dev(lam), dev(mu)
+    dt1 = [torch.zeros_like(db) for _ in range(6)]
+    call("sdmp_elastic_colloc_stress", None, ptrs(dv1), ptrs(dt0), C.c_void_p(dlam.data_ptr()),
+         C.c_void_p(dmu.data_ptr()), ptrs(dt1), *geo, c1t, C.c_float(dt))
+    wt = [np.zeros(full) for _ in range(6)]
+    K.stress_update([f64(x) for x in v1], [f64(x) for x in t0], f64(lam), f64(mu),
+                    [f64(c) for c in c1], dt, box, wt, col=True)
+    for g, w in zip(dt1, wt):
+        assert rel_l2(g.cpu().numpy()[s], w[s]) <= REL
+
+
+def test_rot_update_entry_point():
+    so = 8
+    r = so // 2
+    full = (16 + 4 * so, 16 + 4 * so, 24 + 4 * so)
+    lo, hi = (2 * so,) * 3, tuple(n - 2 * so for n in full)
+    rng = np.random.default_rng(21)
+    u0, u2 = (np.float32(rng.standard_normal(full)) for _ in range(2))
+    m = np.float32(0.2 + 0.2 * rng.random(full))
+    th, ph = rng.random(full) * 0.6, rng.random(full) * 0.6
+    a = [np.float32(np.sin(th) * np.cos(ph)), np.float32(np.sin(th) * np.sin(ph)),
+         np.float32(np.cos(th))]
+    w1 = [float(c) for c in S.fd_coefficients(1, so)]
+    d1 = [np.float32([0.0] + [w1[r + k] / 10.0 for k in range(1, r + 1)]) for _ in range(3)]
+    dt2 = float(np.float32(0.25))
+    ins = [dev(x) for x in (u0, u2, m, *a)]
+    u1 = torch.zeros_like(ins[0])
+    call("sdmp_rot_update", None, ptrs(ins), C.c_void_p(u1.data_ptr()), arr(C.c_int64, full),
+         arr(C.c_int64, lo), arr(C.c_int64, hi), r,
+         R.coeff_table(d1, NC).ctypes.data_as(C.POINTER(C.c_float)), C.c_float(dt2))
+    f64 = lambda x: x.astype(np.float64)
+    want = np.zeros(full)
+    K.rot_update(f64(u0), f64(u2), f64(m), [f64(x) for x in a], [f64(c) for c in d1], dt2,
+                 (lo, hi), want)
+    s = tuple(slice(x, y) for x, y in zip(lo, hi))
+    assert rel_l2(u1.cpu().numpy()[s], want[s]) <= REL
