@@ -3,6 +3,8 @@ out=gpurun_out/family_table.jsonl; rm -f $out
 run() { python bench.py --kernel $1 --so $2 $3 --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 >> $out; }
 for so in 4 8 12 16; do run acoustic $so ""; done
 for so in 4 8 16; do run damped $so ""; done
+for so in 4 8 16; do run rotated $so "--shape 512,512,512"; done
+for so in 8; do run elastic_col $so "--shape 512,512,512"; done
 for k in tti elastic visco; do for so in 4 8 12 16; do run $k $so "--shape 512,512,512"; done; done
 python - <<'PY'
 import json
