@@ -290,6 +290,7 @@ def main():
     # then K timed steps (graph replay, no tracing), then the same K steps
     # again with per-action CUDA-event tracing (untimed) for the breakdown.
     plan = op._native(mode, dt)
+    plan.check_cfl()  # the acoustic CFL guard (collective), once per model
     plan.run(0, args.warmup - 1) if args.warmup > 0 else None
     torch.cuda.synchronize()
     nplan = plan.plan

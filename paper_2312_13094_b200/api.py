@@ -580,6 +580,7 @@ class Operator:
             time_M = min(nts) - 1
         mode = CP.normalise_mode(mpi or kwargs.get("mode") or _env_mode())
         plan = self._native(mode, dt)
+        plan.check_cfl()  # collective: apply is called by every rank
         t0 = _time.perf_counter()
         plan.run(int(time_m), int(time_M))
         torch.cuda.synchronize()

@@ -135,6 +135,7 @@ class NativeOperatorPlan:
 
         # -- bound parameters ------------------------------------------------
         self.scale_bufs = []  # (out tensor, m tensor, C)
+        self.cfl = []         # (StarKernel, m Function): acoustic CFL guard
         self.var_bufs = []    # (VarStarKernel, u Function, {"A"|"B"|"S": tensor})
         self.kparams = {}
         spacing = grid.spacing
@@ -147,6 +148,8 @@ class NativeOperatorPlan:
                     mfn = op.fields[k.m]
                     sbuf = torch.empty_like(mfn.storage[0])
                     self.scale_bufs.append((sbuf, mfn, C))
+                    if (k.A, k.B, k.p, k.q) == (2, -1, 2, -1):
+                        self.cfl.append((k, mfn))
                     mid = self.plan.add_field([int(sbuf.data_ptr())], mfn.full3)
                     variant = R.VARIANT_M_IS_SCALE
                     self.keep.append(sbuf)
@@ -413,6 +416,38 @@ class NativeOperatorPlan:
                 self._seen["static"] = ver
         self.plan.run(time_m, time_M)
         self.plan.sync()
+
+    def check_cfl(self):
+        """Collective (every rank calls it from Operator.apply): re-check the
+        acoustic CFL guard whenever m changed."""
+        for k, mfn in self.cfl:
+            if self._seen.get(("cfl", id(k))) != mfn._version:
+                self._check_cfl(k, mfn)
+                self._seen[("cfl", id(k))] = mfn._version
+
+    def _check_cfl(self, k, mfn):
+        """Acoustic CFL guard: refuse a dt above the
+        leapfrog stability limit of this stencil, dt_max = 2 / (v_max
+        sqrt(lambda_max)) with lambda_max = sum_a |w_0 + 2 sum_k (-1)^k w_k| /
+        h_a^2 (the stencil's symbol at the Nyquist wavenumber) and
+        v_max = 1 / sqrt(min m) over the global domain."""
+        c = float(k.c)
+        if self.dt is None or c <= 0:
+            return
+        m_min = float(mfn._domain_view(0).min())
+        m_min = -self.ctx.allreduce_max(-m_min)
+        if m_min <= 0:
+            raise ValueError("acoustic model has m <= 0 (m = 1/vp^2 must be positive)")
+        lam = 0.0
+        for w, h in zip(k.weights, self.op.grid.spacing):
+            sym = float(w[0]) + 2.0 * sum(float(w[j]) * (-1) ** j for j in range(1, len(w)))
+            lam += abs(sym) / (h * h)
+        dt_max = 2.0 / (math.sqrt(c * lam / m_min))
+        if float(self.dt) > dt_max * (1.0 + 1e-6):
+            raise ValueError(
+                f"dt = {float(self.dt):.6g} exceeds the CFL stability limit {dt_max:.6g} of "
+                f"this SO-{k.u.space_order} acoustic stencil (v_max = {1 / math.sqrt(m_min):.4g}); "
+                "reduce dt (kernels.critical_dt gives a conservative choice)")
 
     def _bind_var(self, k, ufn, bufs, max_points: int = 1 << 26):
         """A, B, S of a variable-coefficient star from its static fields:

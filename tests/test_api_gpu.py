@@ -241,7 +241,7 @@ def test_static_field_update_between_applies():
         u.data[:, 10, 10, 14] = 1.0
         return u, m, Operator([kd])
 
-    dt = float(np.float32(KD.critical_dt(4.6, (10.0,) * 3)))
+    dt = float(np.float32(KD.critical_dt(4.6 * 1.5, (10.0,) * 3)))  # stable for m / 2 too
     u1, m1, op1 = build("sv1")
     op1.apply(time_M=0, dt=dt)           # binds dt^2/m with the original m
     m1.data[...] = m1.data[...] * np.float32(0.5)
@@ -359,3 +359,16 @@ def test_collocated_elastic_vs_oracle(so):
         err = rel_l2(got, want)
         assert err <= REL, (name, err, np.abs(got - want).max())
     assert np.abs(sim.gather("vx", steps % 2)).max() > 0
+
+
+def test_acoustic_cfl_guard():
+    """a dt above the stencil's leapfrog stability limit is
+    refused at configuration time; the conservative critical_dt runs."""
+    shape = (24, 20, 28)
+    grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
+    kd = KD.acoustic_model(grid, so=8, name="u_cfl")
+    op = Operator([kd])
+    vmax = float(1.0 / np.sqrt(kd.fields["m"].data_gather().min()))
+    with pytest.raises(ValueError, match="CFL"):
+        op.apply(time_M=1, dt=0.6 * 10.0 / vmax)
+    op.apply(time_M=1, dt=float(np.float32(KD.critical_dt(vmax, grid.spacing))))

@@ -34,6 +34,15 @@ def test_two_gpus_all_families(topo, shape):
     assert rep["results"] and all(v["equal"] for v in rep["results"].values()), rep
 
 
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 3,
+                    reason="needs >= 3 GPUs")
+def test_three_gpus_odd_rank_count():
+    # SPEC acceptance matrix includes 3 ranks: uneven split along x
+    rc, rep, err = _run(3, "3,1,1", "50,36,32", "acoustic,damped,rotated,tti,elastic_col,visco")
+    assert rc == 0, (rep, err)
+    assert all(v["equal"] for v in rep["results"].values()), rep
+
+
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
                     reason="needs >= 4 GPUs")
 def test_four_gpus_x_interior_ranks():
