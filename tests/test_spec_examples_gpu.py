@@ -59,3 +59,23 @@ def test_elastic_zero_state_stays_zero():
     Operator([kd]).apply(time_M=4, dt=float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.1))))
     for n in KD.VNAMES + KD.TNAMES:
         assert not np.any(kd.fields[n].data_gather())
+
+
+def test_spec_pack_unpack_round_trip():
+    """pack then unpack into an equal box of a zeroed field
+    reproduces the values (row-major); empty box -> empty buffer."""
+    from paper_2312_13094_b200 import api, spec as SP
+    g = S.GridSpec((12, 10, 16), (110.0, 90.0, 150.0))
+    a = SP.allocate(S.FieldSpec("pk_a", g, 4, 0), comm="self")
+    b = SP.allocate(S.FieldSpec("pk_b", g, 4, 0), comm="self")
+    a.storage.copy_(torch.randn_like(a.storage))
+    box = ((3, 2, 5), (9, 7, 13))
+    buf = SP.pack_region(a, box)
+    assert buf.numel() == 6 * 5 * 8
+    ref = a.storage[0][3:9, 2:7, 5:13].reshape(-1)
+    assert torch.equal(buf, ref)
+    SP.unpack_region(b, box, buf)
+    assert torch.equal(b.storage[0][3:9, 2:7, 5:13], a.storage[0][3:9, 2:7, 5:13])
+    assert SP.pack_region(a, ((3, 2, 5), (3, 7, 13))).numel() == 0
+    with pytest.raises(ValueError):
+        SP.unpack_region(b, box, buf[:-1])
