@@ -317,6 +317,7 @@ struct StressOpT {
 struct ViscoOp {
   static constexpr int NF = 3, NC = 3, NP = 15;
   static constexpr int kCtas = SDMP_VISCO_CTAS;
+  static constexpr int kUnrollMinR = 5;  // unroll_for: U = 1 below SO-10 (r03 A/B)
   float* out[12];
   ElCoef k;
   template <int R, class Ctx>

@@ -356,6 +356,11 @@ struct TmaCfg {
 #ifndef SDMP_STAR_RING_MIN
 #define SDMP_STAR_RING_MIN 1
 #endif
+#ifndef SDMP_TMA2_UNROLL
+#define SDMP_TMA2_UNROLL 2
+#endif
+constexpr int kTma2Unroll = SDMP_TMA2_UNROLL;
+
 template <int R>
 constexpr bool kStarRing = R >= SDMP_STAR_RING_MIN && R <= 4;  // r02 A/B: wide stencils lose
 
@@ -616,22 +621,16 @@ star_tma2(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ 
   const bool zin = z < p.g.hi[2];
   const bool act0 = zin && (y0 + r0 < p.g.hi[1]), act1 = zin && (y0 + r0 + 1 < p.g.hi[1]);
   constexpr int W = 2 * R + 1;
-  float4 w0[W], w1[W];
+  // x-windows unrolled by U planes: plane slots are constants inside the
+  // unrolled group and the 2R live planes move down once per group (2R / U
+  // register moves per plane instead of 2R; r03 A/B, SDMP_TMA2_UNROLL)
+  constexpr int U = kTma2Unroll;
+  float4 w0[W + U - 1], w1[W + U - 1];
 #pragma unroll
-  for (int k = 0; k < W; ++k) w0[k] = w1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k = 0; k < W + U - 1; ++k) w0[k] = w1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
 
-  for (int i = 0; i < nit; ++i) {
-    const int s = i % T::S;
-    mbar_wait(&full_bar[s], (i / T::S) & 1);
-    const unsigned char* st = sm + s * T::STAGE;
-    const float* front = reinterpret_cast<const float*>(st) + 4 * lane;
-#pragma unroll
-    for (int k = 0; k < 2 * R; ++k) {
-      w0[k] = w0[k + 1];
-      w1[k] = w1[k + 1];
-    }
-    w0[2 * R] = *reinterpret_cast<const float4*>(front + r0 * kTZ);
-    w1[2 * R] = *reinterpret_cast<const float4*>(front + (r0 + 1) * kTZ);
+  // one x-plane: window slots b .. b + 2R (b = group position, a constant)
+  auto consume = [&](const int i, const int b, const unsigned char* st) {
     if (i >= 2 * R && (act0 || act1)) {
       const int x = xa + i - 2 * R;
       // centre tile row (r0 + R + d) at this thread's 4 z points
@@ -641,15 +640,15 @@ star_tma2(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ 
       V2 l0[2], l1[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        l0[h] = vcmul(p.csum0, f4pair(w0[R], h));
-        l1[h] = vcmul(p.csum0, f4pair(w1[R], h));
+        l0[h] = vcmul(p.csum0, f4pair(w0[b + R], h));
+        l1[h] = vcmul(p.csum0, f4pair(w1[b + R], h));
       }
 #pragma unroll
       for (int k = 1; k <= R; ++k)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          l0[h] = vcfma(p.c[0][k], vadd(f4pair(w0[R - k], h), f4pair(w0[R + k], h)), l0[h]);
-          l1[h] = vcfma(p.c[0][k], vadd(f4pair(w1[R - k], h), f4pair(w1[R + k], h)), l1[h]);
+          l0[h] = vcfma(p.c[0][k], vadd(f4pair(w0[b + R - k], h), f4pair(w0[b + R + k], h)), l0[h]);
+          l1[h] = vcfma(p.c[0][k], vadd(f4pair(w1[b + R - k], h), f4pair(w1[b + R + k], h)), l1[h]);
         }
       // y taps: row 0 uses rows -k / +k, row 1 rows 1-k / 1+k (k ascending
       // for each): A_k = row(-k), B_k = row(+k); row 1 at k takes
@@ -686,12 +685,33 @@ star_tma2(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ 
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
         const float4 mv = has_m ? *reinterpret_cast<const float4*>(pts + T::FRONT / 4 + rr * kTZ)
                                 : make_float4(1.f, 1.f, 1.f, 1.f);
-        star_finish4(p, l, j == 0 ? w0[R] : w1[R], u2v, mv, out);
+        star_finish4(p, l, j == 0 ? w0[b + R] : w1[b + R], u2v, mv, out);
         if (j == 0 ? act0 : act1) star_store4(p, push, x, y0 + rr, z, out);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[s]);
+  };
+
+  for (int i0 = 0; i0 < nit; i0 += U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u;
+      if (i < nit) {
+        const int s = i % T::S;
+        mbar_wait(&full_bar[s], (i / T::S) & 1);
+        const unsigned char* st = sm + s * T::STAGE;
+        const float* front = reinterpret_cast<const float*>(st) + 4 * lane;
+        w0[2 * R + u] = *reinterpret_cast<const float4*>(front + r0 * kTZ);
+        w1[2 * R + u] = *reinterpret_cast<const float4*>(front + (r0 + 1) * kTZ);
+        consume(i, u, st);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2 * R; ++k) {
+      w0[k] = w0[k + U];
+      w1[k] = w1[k + U];
+    }
   }
 }
 

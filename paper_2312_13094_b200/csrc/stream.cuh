@@ -82,6 +82,26 @@ constexpr int ctas_for() {
   return TY + 1 <= 9 ? CtasOf<Op>::value : 1;
 }
 
+// x-window unroll (stream_kernel): U = 2 planes per group where it was
+// measured faster (r03 A/B: TTI, elastic SO-16, visco SO-16, damped +1-7%),
+// 1 for ops that declare Op::kUnrollMinR above R (visco stress at SO-8 lost
+// 15% to register pressure).  SDMP_STREAM_UNROLL overrides (development).
+#ifndef SDMP_STREAM_UNROLL
+#define SDMP_STREAM_UNROLL 0
+#endif
+template <class Op, class = void>
+struct UnrollMinR {
+  static constexpr int value = 0;
+};
+template <class Op>
+struct UnrollMinR<Op, std::void_t<decltype(Op::kUnrollMinR)>> {
+  static constexpr int value = Op::kUnrollMinR;
+};
+template <class Op, int R>
+constexpr int unroll_for() {
+  return SDMP_STREAM_UNROLL ? SDMP_STREAM_UNROLL : (R >= UnrollMinR<Op>::value ? 2 : 1);
+}
+
 template <int V> struct VType;
 template <> struct VType<1> { using T = float; };
 template <> struct VType<2> { using T = V2; };
@@ -98,20 +118,20 @@ __device__ __forceinline__ V2 vload<2>(const float* p) {
 }
 
 // Consumer-side view of one thread's V points.
-template <int R, int TY, int V, int NF, int NC, int NP>
+template <int R, int TY, int V, int NF, int NC, int NP, int U = 1>
 struct StreamCtx {
   using L = SLayout<R, TY, V, NF, NC, NP>;
   using T = typename VType<V>::T;
   static constexpr int W = 2 * R + 1;
-  const T (*w)[W];   // x-windows (register ring)
+  static constexpr int WB = W + U - 1;
+  const T (*w)[WB];  // x-windows (registers, see stream_kernel)
   const unsigned char* stage;
   int warp, lane;
-  int rot;           // ring rotation = iteration % W (a constant after unrolling)
+  int base;          // window slot of plane x - R (a constant after unrolling)
   const Push* push;  // fused halo push (full mode OWNED slabs), ndir 0 = none
   int x, y, z;       // FULL coordinates of the thread's first point
-  // plane x + k of front field f: loaded at iteration i - R + k, ring slot
-  // (i - R + k) mod W = (rot + R + 1 + k) mod W
-  __device__ __forceinline__ T xt(int f, int k) const { return w[f][(rot + R + 1 + k) % W]; }
+  // plane x + k of front field f
+  __device__ __forceinline__ T xt(int f, int k) const { return w[f][base + R + k]; }
   __device__ __forceinline__ const float* crow(int c, int dy) const {
     const float* base = reinterpret_cast<const float*>(stage + NF * L::FRONT + c * L::CENTER);
     return base + (warp + R + dy) * L::CZ + L::OFF + V * lane;
@@ -251,33 +271,41 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
   const bool m1 = V > 1 && yin && z + 1 >= g.lo[2] && z + 1 < g.hi[2];
   const bool active = m0 || m1;
   constexpr int W = 2 * R + 1;
-  T w[NF > 0 ? NF : 1][W];
+  // x-windows unrolled by U planes: slots are constants inside the unrolled
+  // group and the 2R live planes move down once per group (2R / U register
+  // moves per plane instead of 2R; unroll_for)
+  constexpr int U = unroll_for<Op, R>();
+  T w[NF > 0 ? NF : 1][W + U - 1];
 #pragma unroll
   for (int f = 0; f < NF; ++f)
 #pragma unroll
-    for (int k = 0; k < W; ++k) w[f][k] = vconst<T>(0.f);
+    for (int k = 0; k < W + U - 1; ++k) w[f][k] = vconst<T>(0.f);
 
-  {
-    // sliding window: newest plane at slot 2R (rotation W - 1)
-    for (int i = 0; i < nit; ++i) {
-      const int s = i % L::S;
-      mbar_wait(&full_bar[s], (i / L::S) & 1);
-      const unsigned char* st = sm + s * L::STAGE;
+  for (int i0 = 0; i0 < nit; i0 += U) {
 #pragma unroll
-      for (int f = 0; f < NF; ++f) {
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u;
+      if (i < nit) {
+        const int s = i % L::S;
+        mbar_wait(&full_bar[s], (i / L::S) & 1);
+        const unsigned char* st = sm + s * L::STAGE;
 #pragma unroll
-        for (int k = 0; k < 2 * R; ++k) w[f][k] = w[f][k + 1];
-        w[f][2 * R] = vload<V>(reinterpret_cast<const float*>(st + f * L::FRONT) +
-                               warp * L::TZ + V * lane);
+        for (int f = 0; f < NF; ++f)
+          w[f][2 * R + u] = vload<V>(reinterpret_cast<const float*>(st + f * L::FRONT) +
+                                     warp * L::TZ + V * lane);
+        if (i >= 2 * R && active) {
+          const int x = xa + i - 2 * R;
+          StreamCtx<R, TY, V, NF, NC, NP, U> ctx{w, st, warp, lane, u, &push, x, y, z};
+          op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0, m1);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
       }
-      if (i >= 2 * R && active) {
-        const int x = xa + i - 2 * R;
-        StreamCtx<R, TY, V, NF, NC, NP> ctx{w, st, warp, lane, W - 1, &push, x, y, z};
-        op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0, m1);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+#pragma unroll
+      for (int k = 0; k < 2 * R; ++k) w[f][k] = w[f][k + U];
   }
 }
 
