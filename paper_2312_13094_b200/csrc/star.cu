@@ -356,6 +356,9 @@ struct TmaCfg {
 #ifndef SDMP_STAR_RING_MIN
 #define SDMP_STAR_RING_MIN 1
 #endif
+#ifndef SDMP_TMA2_TY8
+#define SDMP_TMA2_TY8 14  // rows per CTA of star_tma2<8> (A/B)
+#endif
 #ifndef SDMP_TMA2_UNROLL
 #define SDMP_TMA2_UNROLL 2
 #endif
@@ -867,7 +870,7 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
     switch (R) {
       case 6: return launch_tma2<6, 16>(p, st, full, push);
       case 7: return launch_tma2<7, 16>(p, st, full, push);
-      case 8: return launch_tma2<8, 14>(p, st, full, push);
+      case 8: return launch_tma2<8, SDMP_TMA2_TY8>(p, st, full, push);
     }
   }
   if (variant == 7) {  // A/B
