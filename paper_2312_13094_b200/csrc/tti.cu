@@ -366,10 +366,21 @@ static int launch_tti_stream(const Op& op, const Geom& g, const int64_t full[3],
     if (ny <= 8) return launch_stream_op<R, 8, VG>(op, g, full, arrs, st, push);
     return launch_stream_op<R, upd ? SDMP_UOP_TY : SDMP_GOP_TY, VG>(op, g, full, arrs, st, push);
   } else {
-    // r02 A/B (512^3): update pass with one point per thread and 16-row
-    // tiles from R = 6 (SO-12 35.7 -> 43.3 GPts/s), g pass 16 rows at R = 6
-    constexpr int TYW = upd ? (R == 5 ? 8 : 16) : (R <= 6 ? 16 : 8);
-    constexpr int VW = (!upd || R == 5) ? 2 : 1;
+    // r02 A/B (512^3): g pass 16 rows at R = 5-6
+    // r03 A/B (tools/ab_ttiw.sh, 512^3, under the x-window unroll): update
+    // pass 8 rows x 2 points from R = 5 (SO-12 45.4 -> 48.2, SO-16 33.9 ->
+    // 35.4), g pass 12 rows at R = 7-8 (SO-16 +2.5%)
+#ifndef SDMP_TTI_GTYW
+#define SDMP_TTI_GTYW 12
+#endif
+#ifndef SDMP_TTI_UTYW
+#define SDMP_TTI_UTYW 8
+#endif
+#ifndef SDMP_TTI_UVW
+#define SDMP_TTI_UVW 2
+#endif
+    constexpr int TYW = upd ? SDMP_TTI_UTYW : (R <= 6 ? 16 : SDMP_TTI_GTYW);
+    constexpr int VW = upd ? SDMP_TTI_UVW : 2;
     if (ny <= 8) return launch_stream_op<R, 8, VW>(op, g, full, arrs, st, push);
     return launch_stream_op<R, TYW, VW>(op, g, full, arrs, st, push);
   }
@@ -513,18 +524,35 @@ static int launch_rot(TTIGeneric& p, cudaStream_t st, const int64_t full[3], con
   const bool stream = variant_env() != 1 && stream_fits(p1.g, R) && stream_fits(p.g, R) &&
                       tma_ok(full, a1, 5) && tma_ok(full, a2, 8);
   if (stream) {
-    constexpr int TY = R <= 4 ? 16 : 8;
+    // r03 A/B (tools/ab_rot.sh, 512^3): g pass 8 rows at R = 3-4 (SO-8
+    // 104.6 -> 110.9 GPts/s; SO-4 keeps 16), both passes 12 rows above R = 4
+    // (SO-16 64.4 -> 76.6)
+#ifndef SDMP_RG_TYN
+#define SDMP_RG_TYN 8
+#endif
+#ifndef SDMP_RG_TYW
+#define SDMP_RG_TYW 12
+#endif
+#ifndef SDMP_RU_TYN
+#define SDMP_RU_TYN 16
+#endif
+#ifndef SDMP_RU_TYW
+#define SDMP_RU_TYW 12
+#endif
+    constexpr int TYG = R <= 2 ? 16 : R <= 4 ? SDMP_RG_TYN : SDMP_RG_TYW;
+    constexpr int TYU = R <= 4 ? SDMP_RU_TYN : SDMP_RU_TYW;
+    constexpr int VU = 2;
     RGOp g{};
     g.out = p1.out[0];
     g.k = p.c;
-    int rc = launch_stream_op<R, TY, 2>(g, p1.g, full, a1, st);
+    int rc = launch_stream_op<R, TYG, 2>(g, p1.g, full, a1, st);
     if (rc) return rc;
     RUOp u{};
     u.out = p.out[0];
     u.k = p.c;
     const int ny = p.g.hi[1] - p.g.lo[1];
     if (ny <= 8) return launch_stream_op<R, 8, 2>(u, p.g, full, a2, st, &push);
-    return launch_stream_op<R, TY, 2>(u, p.g, full, a2, st, &push);
+    return launch_stream_op<R, TYU, VU>(u, p.g, full, a2, st, &push);
   }
   dim3 b(32, 8);
   dim3 g1((p1.g.hi[2] - p1.g.lo[2] + 31) / 32, (p1.g.hi[1] - p1.g.lo[1] + 7) / 8,
