@@ -194,15 +194,32 @@ __device__ __forceinline__ void push_vals(const Push& P, int x, int y, int z, co
 }
 
 // masked store of V consecutive values at idx (m0: first point, m1: second)
+// Output stores.  SDMP_STREAM_CS = 1 marks them evict-first (st.global.cs):
+// every output array is far larger than L2, so keeping it out of L2 leaves
+// room for the halo tiles neighbouring CTAs re-read.
+#ifndef SDMP_STREAM_CS
+#define SDMP_STREAM_CS 0
+#endif
+__device__ __forceinline__ void st_out(float* p, float v) {
+#if SDMP_STREAM_CS
+  asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v));
+#else
+  *p = v;
+#endif
+}
 __device__ __forceinline__ void vstore(float* p, int64_t idx, float v, bool m0, bool) {
-  if (m0) p[idx] = v;
+  if (m0) st_out(p + idx, v);
 }
 __device__ __forceinline__ void vstore(float* p, int64_t idx, V2 v, bool m0, bool m1) {
   if (m0 && m1) {
+#if SDMP_STREAM_CS
+    asm volatile("st.global.cs.b64 [%0], %1;" ::"l"(p + idx), "l"(v.r));
+#else
     *reinterpret_cast<uint64_t*>(p + idx) = v.r;
+#endif
   } else {
-    if (m0) p[idx] = v2lo(v);
-    if (m1) p[idx + 1] = v2hi(v);
+    if (m0) st_out(p + idx, v2lo(v));
+    if (m1) st_out(p + idx + 1, v2hi(v));
   }
 }
 
