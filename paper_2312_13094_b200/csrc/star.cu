@@ -513,7 +513,12 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
 
 // Pick the number of x chunks: whole waves of one CTA per SM, small
 // priming overhead (2R front-only iterations per chunk).
-static int pick_chunks(int64_t tiles, int nx, int R, int ctas_per_sm) {
+// cost of n x-chunks = waves x (chunk planes + x-window fill + per-CTA fixed
+// cost `cta_planes`, in plane units).  star_tma: 4 planes (prologue, tensor-map
+// prefetch, pipeline fill / drain) -- at C1's 256^3 one wave of 64-plane-chunk
+// CTAs beats two waves of 29-plane chunks by 5% (profiles/r03_ab_nch.log);
+// 512^3 and 1024^3 keep their choices.
+static int pick_chunks(int64_t tiles, int nx, int R, int ctas_per_sm, double cta_planes = 0.0) {
   const int64_t slots = (int64_t)num_sms() * ctas_per_sm;
   double best = 1e30;
   int best_n = 1;
@@ -521,7 +526,7 @@ static int pick_chunks(int64_t tiles, int nx, int R, int ctas_per_sm) {
     const int chunk = (nx + n - 1) / n;
     const int64_t items = tiles * ((nx + chunk - 1) / chunk);
     const int64_t waves = (items + slots - 1) / slots;
-    const double cost = (double)waves * (chunk + 0.35 * 2 * R);
+    const double cost = (double)waves * (chunk + 0.35 * 2 * R + cta_planes);
     if (cost < best - 1e-9) {
       best = cost;
       best_n = n;
@@ -550,7 +555,8 @@ static int launch_tma(const StarParams& p, cudaStream_t st, const int64_t full[3
   if (rc) return rc;
   const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
   const int tz = (nz + kTZ - 1) / kTZ, ty = (ny + TY - 1) / TY;
-  int nch = pick_chunks((int64_t)tz * ty, nx, R, 1);
+  int nch = pick_chunks((int64_t)tz * ty, nx, R, 1, 4.0);
+  if (const char* e = getenv("SDMP_STAR_NCH")) nch = std::max(1, std::min(nx, atoi(e)));  // A/B
   const int chunk = (nx + nch - 1) / nch;
   nch = (nx + chunk - 1) / chunk;
   SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");
