@@ -329,13 +329,17 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
 // x-chunk count: whole waves of one CTA per SM, small priming overhead.
 inline int stream_chunks(int64_t tiles, int nx, int R, int ctas = 1) {
   const int64_t slots = (int64_t)num_sms() * ctas;
+  static const double cta_planes = [] {  // A/B: per-CTA fixed cost in planes
+    const char* e = getenv("SDMP_STREAM_CTA_PLANES");
+    return e ? atof(e) : 0.0;
+  }();
   double best = 1e30;
   int best_n = 1;
   for (int n = 1; n <= 64 && n <= nx; ++n) {
     const int chunk = (nx + n - 1) / n;
     const int64_t items = tiles * ((nx + chunk - 1) / chunk);
     const int64_t waves = (items + slots - 1) / slots;
-    const double cost = (double)waves * (chunk + 0.5 * 2 * R);
+    const double cost = (double)waves * (chunk + 0.5 * 2 * R + cta_planes);
     if (cost < best - 1e-9) {
       best = cost;
       best_n = n;
