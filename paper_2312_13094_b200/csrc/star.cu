@@ -537,7 +537,7 @@ static int pick_chunks(int64_t tiles, int nx, int R, int ctas_per_sm, double cta
 
 template <int R, int TY>
 static int launch_tma(const StarParams& p, cudaStream_t st, const int64_t full[3],
-                      const Push& push) {
+                      const Push& push, int ctas = 1) {
   using T = TmaCfg<R, TY>;
   static int attr_dev = -1;
   int dev = 0;
@@ -555,7 +555,7 @@ static int launch_tma(const StarParams& p, cudaStream_t st, const int64_t full[3
   if (rc) return rc;
   const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
   const int tz = (nz + kTZ - 1) / kTZ, ty = (ny + TY - 1) / TY;
-  int nch = pick_chunks((int64_t)tz * ty, nx, R, 1, 4.0);
+  int nch = pick_chunks((int64_t)tz * ty, nx, R, ctas, 4.0);
   if (const char* e = getenv("SDMP_STAR_NCH")) nch = std::max(1, std::min(nx, atoi(e)));  // A/B
   const int chunk = (nx + nch - 1) / nch;
   nch = (nx + chunk - 1) / chunk;
@@ -877,6 +877,12 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
       case 6: return launch_tma2<6, 16>(p, st, full, push);
       case 7: return launch_tma2<7, 16>(p, st, full, push);
       case 8: return launch_tma2<8, SDMP_TMA2_TY8>(p, st, full, push);
+    }
+  }
+  if (variant == 8) {  // A/B: 8-row tiles, two CTAs per SM (small grids)
+    switch (R) {
+      case 2: return launch_tma<2, 8>(p, st, full, push, 2);
+      case 4: return launch_tma<4, 8>(p, st, full, push, 2);
     }
   }
   if (variant == 7) {  // A/B
