@@ -134,77 +134,119 @@ class ClockSampler:
 # CPU reference arm / baseline: the oracle port (numpy, fp64) on a slab
 
 
-def cpu_reference(n, so, seconds, threads=None, max_steps=None):
-    """Time the oracle's star update (oracle/stencils.star_update, the CPU
-    restatement of the reference path) on a bounded slab of the n^3 workload:
-    x-planes [0, nx) of an n x n cross-section, nx chosen for ~``seconds``.
-    Threads split the slab along x (numpy releases the GIL)."""
-    from concurrent.futures import ThreadPoolExecutor
-    from oracle import stencils as K
-    from paper_2312_13094_b200.symbolics import fd_coefficients
-    r = so // 2
-    threads = threads or os.cpu_count() or 1
-    w = [float(c) for c in fd_coefficients(2, so)]
-    h = 10.0
-    coeffs = [np.float32([w[r + k] / (h * h) for k in range(r + 1)]).astype(np.float64)] * 3
-    nx = max(threads * 2, 8)
-    ny = nz = n
-    full = (nx + 2 * so, ny + 2 * so, nz + 2 * so)
-    rng = np.random.default_rng(0)
-    u0 = rng.standard_normal(full)
-    u2 = rng.standard_normal(full)
-    m = np.full(full, 0.25)
-    out = np.zeros(full)
-    chunks = np.array_split(np.arange(so, so + nx), threads)
+class CpuSlab:
+    """The oracle port of one configured step (oracle/stencils: star update,
+    source injection, receiver interpolation -- the CPU restatement of the
+    reference path) on a bounded slab of the n^3 workload: x-planes [0, nx)
+    of the full n x n cross-section with a Ricker source and a receiver line
+    inside the slab.  Arrays are allocated and filled ONCE (``__init__``);
+    ``step()`` is the timed unit.  Threads split the slab along x (numpy
+    releases the GIL)."""
 
-    def work(ix):
-        if len(ix) == 0:
-            return
-        box = ((int(ix[0]), so, so), (int(ix[-1]) + 1, so + ny, so + nz))
-        K.star_update(u0, u2, m, coeffs, 2.0, -1.0, 1e-3, box, out)
+    def __init__(self, n, so, threads=None, nx=None, nrec=256):
+        from concurrent.futures import ThreadPoolExecutor
+        from oracle import stencils as K
+        from paper_2312_13094_b200.symbolics import fd_coefficients
+        self.K = K
+        self.so, r = so, so // 2
+        self.threads = threads or os.cpu_count() or 1
+        w = [float(c) for c in fd_coefficients(2, so)]
+        self.h = h = 10.0
+        self.coeffs = [np.float32([w[r + k] / (h * h) for k in range(r + 1)]).astype(np.float64)] * 3
+        self.nx = nx or max(self.threads * 2, 8)
+        self.ny = self.nz = n
+        full = (self.nx + 2 * so, n + 2 * so, n + 2 * so)
+        rng = np.random.default_rng(0)
+        self.bufs = [rng.standard_normal(full) for _ in range(3)]
+        self.m = np.full(full, 0.25)
+        self.dt2 = 1e-3
+        self.chunks = [c for c in np.array_split(np.arange(so, so + self.nx), self.threads) if len(c)]
+        self.pool = ThreadPoolExecutor(self.threads)
+        shape = (self.nx, n, n)
+        ext = [h * (s_ - 1) for s_ in shape]
+        src = [0.5 * ext[0] + 0.3, 0.5 * ext[1] + 3.7, 0.5 * ext[2] + 3.7]
+        corners, weights = K.trilinear(src, (h, h, h), shape)
+        self.src_nodes = {c: [(0, wt)] for c, wt in zip(corners, weights)}
+        self.rec = [K.trilinear([x, 0.5 * ext[1] + 2.5, 20.3], (h, h, h), shape)
+                    for x in np.linspace(5.0, ext[0] - 5.0, nrec)]
+        self.amps = np.float32(K.ricker(0.010, np.arange(4096) * 1.0, 100.0)).astype(np.float64)
+        self.time = 0
+        self.trace = np.zeros(nrec)
 
-    pool = ThreadPoolExecutor(threads)
+    def step(self):
+        K, so = self.K, self.so
+        u2, u0, u1 = (self.bufs[(self.time + k) % 3] for k in (-1, 0, 1))
+        halo, origin = (so, so, so), (0, 0, 0)
+        for i, (c, wts) in enumerate(self.rec):   # receivers sample u[t]
+            self.trace[i] = K.interpolate(u0, halo, origin, c, wts)
+
+        def work(ix):
+            box = ((int(ix[0]), so, so), (int(ix[-1]) + 1, so + self.ny, so + self.nz))
+            K.star_update(u0, u2, self.m, self.coeffs, 2.0, -1.0, self.dt2, box, u1)
+
+        list(self.pool.map(work, self.chunks))
+        K.inject(u1, halo, origin, self.src_nodes, [self.amps[self.time % len(self.amps)]],
+                 (self.dt2, self.m))
+        self.time += 1
+
+    @property
+    def points(self):
+        return self.nx * self.ny * self.nz
+
+    def sample(self, reps, el):
+        return (f"acoustic SO-{self.so} step (star update + Ricker injection + "
+                f"{len(self.rec)}-receiver interpolation) on a {self.nx}x{self.ny}x{self.nz} "
+                f"slab of the {self.ny}^3 per-GPU grid, {reps} steps in {el:.1f} s, numpy fp64 "
+                f"oracle (oracle/stencils), {self.threads} threads; arrays allocated once, "
+                f"outside the timed loop")
+
+    def close(self):
+        self.pool.shutdown()
+
+
+def cpu_reference(n, so, seconds):
+    """cpu_baseline: CpuSlab steps for ~``seconds`` (after one untimed step)."""
+    slab = CpuSlab(n, so)
+    slab.step()
     t0 = time.perf_counter()
     reps = 0
     while True:
-        list(pool.map(work, chunks))
+        slab.step()
         reps += 1
         el = time.perf_counter() - t0
-        if el >= seconds or (max_steps and reps >= max_steps):
+        if el >= seconds:
             break
-    pool.shutdown()
-    pts = nx * ny * nz * reps
-    return {"value": pts / el / 1e9, "unit": "GPts/s", "cores": threads, "kind": "port",
-            "sample": f"acoustic SO-{so} star update, {nx}x{ny}x{nz} slab of the {n}^3 per-GPU "
-                      f"grid, {reps} sweeps in {el:.1f} s, numpy fp64 oracle "
-                      f"(oracle/stencils.star_update), {threads} threads"}
+    slab.close()
+    return {"value": slab.points * reps / el / 1e9, "unit": "GPts/s", "cores": slab.threads,
+            "kind": "port", "sample": slab.sample(reps, el)}
 
 
 def run_reference(args):
+    """--impl reference: the oracle port (the reference's CPU path restated;
+    the reference itself ships no runtime to install) on the host cores.
+    Each step = one CpuSlab step, W untimed then K timed; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    n = args.n
-    per = cpu_reference(n, args.so, max(2.0, args.cpu_seconds / 3), max_steps=None)
-    # warmup + K "steps" each a bounded slab sample
-    from oracle import stencils  # noqa: F401
-    vals = []
+    slab = CpuSlab(args.n, args.so)
     for _ in range(max(args.warmup, 0)):
-        cpu_reference(n, args.so, 0.1, max_steps=1)
+        slab.step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_reference(n, args.so, 0.1, max_steps=1))
+        slab.step()
     el = time.perf_counter() - t0
-    pts = sum(v["value"] for v in vals) / len(vals)
-    line = {"metric": "GPts/s", "value": pts, "unit": "GPts/s", "impl": "reference",
+    slab.close()
+    val = slab.points * args.steps / el / 1e9
+    line = {"metric": "GPts/s", "value": val, "unit": "GPts/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"acoustic SO-{args.so} {n}^3 per GPU (configs[1]); CPU "
+            "config": {"workload": f"acoustic SO-{args.so} {args.n}^3 per GPU (configs[1]); CPU "
                                    "oracle on a bounded slab per step",
-                       "mode": args.mode},
-            "cpu_baseline": {**per, "value": pts},
-            "e2e": {"value": pts, "unit": "GPts/s", "h2d_bytes_per_step": 0,
+                       "points_per_step": slab.points, "mode": args.mode},
+            "cpu_baseline": {"value": val, "unit": "GPts/s", "cores": slab.threads,
+                             "kind": "port", "sample": slab.sample(args.steps, el)},
+            "e2e": {"value": val, "unit": "GPts/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -220,9 +262,15 @@ def main():
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.warmup < 1:
+        raise SystemExit("--warmup must be >= 1 (the first run binds the plan's derived buffers)")
+    from paper_2312_13094_b200.dist import default_backend
     if world > 1 and not dist.is_initialized():
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+        local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
+        torch.cuda.set_device(local)
+        backend = default_backend()
+        kw = {"device_id": torch.device("cuda", local)} if backend == "nccl" else {}
+        dist.init_process_group(backend, **kw)
     from paper_2312_13094_b200 import Grid, Operator, SparseTimeFunction
     from paper_2312_13094_b200 import kernels as KD
     from paper_2312_13094_b200 import symbolics as S
@@ -291,7 +339,7 @@ def main():
     # again with per-action CUDA-event tracing (untimed) for the breakdown.
     plan = op._native(mode, dt)
     plan.check_cfl()  # the acoustic CFL guard (collective), once per model
-    plan.run(0, args.warmup - 1) if args.warmup > 0 else None
+    plan.run(0, args.warmup - 1)
     torch.cuda.synchronize()
     nplan = plan.plan
     stream = torch.cuda.current_stream()
@@ -469,12 +517,20 @@ def main():
             "rank_actions": rank_actions,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
+    ctx.barrier()
+    # release the plans (IPC mappings, streams, graphs) before the process
+    # group goes away, then exit normally
+    del op, plan, nplan
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    if world > 1 and dist.is_initialized():
+        dist.destroy_process_group()
     return 0
 
 
 if __name__ == "__main__":
     rc = main()
     sys.stdout.flush()
-    os._exit(rc or 0)
+    sys.exit(rc or 0)

@@ -137,6 +137,11 @@ class Data:
         tsel, region, _sq = self._split(key)
         ext = fn.grid.local_extent
         loc = DC.global_to_local(ext, region)
+        # the write is collective: every rank bumps the
+        # version, including ranks the region misses, so the plans' "static
+        # field changed" decisions (collective CFL check, static halo
+        # re-exchange) agree across ranks
+        fn._version += 1
         if loc is None:
             return
         val = value
@@ -154,7 +159,6 @@ class Data:
                 fn.storage.device)
             if fn.grid.ndims == 2:
                 val = val.unsqueeze(-1)
-        fn._version += 1
         for b in self._buffers(tsel, True):
             view = fn._domain_view(b)
             sl = tuple(slice(l, h) for l, h in loc)
@@ -241,8 +245,10 @@ class Function:
         self.grid = grid
         self.spec = S.FieldSpec(name=name, grid=grid.spec, space_order=space_order,
                                 time_order=time_order, halo=halo)
-        if self.spec in _FUNCS:
-            raise ValueError(f"a field named {name!r} with the same spec already exists")
+        # Devito-style re-definition: a new field with the same name and spec
+        # (e.g. a script that rebuilds its Grid / TimeFunction) replaces the
+        # registry entry; Operators built earlier keep the Function objects
+        # they resolved, equations built afterwards bind to the newest one.
         _FUNCS[self.spec] = self
         nd = grid.ndims
         # device layout: halo per side = FieldSpec.halo, except that the z

@@ -24,9 +24,8 @@ class RankContext:
         self.dist = dist if dist.is_available() and dist.is_initialized() else None
         if self.dist is None and int(os.environ.get("WORLD_SIZE", "1")) > 1:
             import torch.distributed as d
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            d.init_process_group(backend=backend)
+            d.init_process_group(backend=default_backend())
             self.dist = d
         if self.dist is not None:
             self.rank = self.dist.get_rank()
@@ -58,6 +57,22 @@ class RankContext:
         if self.size == 1:
             return value
         return max(self.allgather(value))
+
+
+def default_backend() -> str:
+    """Process-group backend for the control plane.  NCCL when every rank
+    has its own GPU; gloo on CPU and when ranks are oversubscribed onto fewer
+    GPUs (NCCL rejects two ranks on one device; the halo data plane is CUDA
+    IPC either way, which works between processes sharing a device).
+    ``SDMP_DIST_BACKEND`` overrides."""
+    import torch
+    forced = os.environ.get("SDMP_DIST_BACKEND")
+    if forced:
+        return forced
+    if not torch.cuda.is_available():
+        return "gloo"
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    return "nccl" if world <= torch.cuda.device_count() else "gloo"
 
 
 class SelfContext(RankContext):

@@ -101,6 +101,49 @@ def elastic(grid, tag, steps, so=8, visco=False, collocated=False):
     return op, dt, [kd.fields[n] for n in names], rec
 
 
+def full_order(op, dt, steps):
+    """Device trace of two more full-mode steps: per phase, the post starts
+    before the wait ends, CORE starts no later than the first OWNED slab, and
+    every OWNED slab starts after the wait ended (Listing 8, SPEC.md:366,
+    450-458; acceptance 8)."""
+    nat = op._native("full", dt)
+    nat.plan.set_tracing(True)
+    nat.plan.run(steps, steps + 1, torch.cuda.current_stream())
+    nat.plan.sync()
+    nat.plan.set_tracing(False)
+    rows = nat.plan.trace()
+    eps = 2e-3
+    problems = []
+    phases = {}
+    cur = 0
+    for i, a in enumerate(nat.eplan.actions):
+        if a.kind == "post":
+            cur = a.phase
+        j = nat.native_index[i]
+        if j < 0:
+            continue
+        beg, dur = rows[j][3], rows[j][4]
+        key = None
+        if a.kind in ("post", "wait"):
+            key = a.kind
+        elif a.kind == "compute" and getattr(a, "region", None) in ("CORE", "OWNED"):
+            key = a.region
+        if key:
+            phases.setdefault(cur, {}).setdefault(key, []).append((beg, beg + dur))
+    for ph, d in phases.items():
+        if "wait" not in d or "OWNED" not in d:
+            continue
+        wait_end = max(e for _b, e in d["wait"])
+        own_beg = min(b for b, _e in d["OWNED"])
+        if own_beg + eps < wait_end:
+            problems.append(f"phase {ph}: OWNED starts {own_beg:.4f} before the wait ends {wait_end:.4f}")
+        if "CORE" in d and min(b for b, _e in d["CORE"]) > own_beg + eps:
+            problems.append(f"phase {ph}: CORE starts after OWNED")
+        if "post" in d and min(b for b, _e in d["post"]) > wait_end + eps:
+            problems.append(f"phase {ph}: post starts after the wait ended")
+    return problems
+
+
 def main():
     ctx = context()
     rank, size = ctx.rank, ctx.size
@@ -108,6 +151,7 @@ def main():
     shape = tuple(int(x) for x in os.environ.get("SHAPE", "40,36,32").split(","))
     steps = int(os.environ.get("STEPS", "12"))
     failures = []
+    order_problems = []
     results = {}
     cases = [("acoustic", acoustic, {}), ("diffusion", diffusion, {}), ("damped", damped, {}),
              ("rotated", rotated, {}), ("tti", tti, {}),
@@ -127,6 +171,8 @@ def main():
             op.apply(time_M=steps - 1, dt=dt, mpi=mode)
             got = [f.data_gather() for f in fields]
             got_tr = rec.data.copy() if rec is not None else None
+            if mode == "full" and size > 1:
+                order_problems.extend(f"{fam}: {p}" for p in full_order(op, dt, steps))
             # release the distributed fields before building the reference
             import paper_2312_13094_b200.api as A
             names_mr = [f.name for f in fields]
@@ -146,10 +192,13 @@ def main():
             del rop, rfields, rrec
             A._FUNCS.clear()
             torch.cuda.empty_cache()
+    orders = ctx.allgather(order_problems)
     if rank == 0:
-        print(json.dumps({"topology": topo, "shape": shape, "results": results}))
+        print(json.dumps({"topology": topo, "shape": shape, "results": results,
+                          "order_ok": not any(orders), "order": orders,
+                          "devices": torch.cuda.device_count(), "ranks": size}))
     ctx.barrier()
-    return 1 if failures else 0
+    return 1 if failures or any(orders) else 0
 
 
 if __name__ == "__main__":

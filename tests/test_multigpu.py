@@ -1,6 +1,18 @@
-"""Multi-GPU bitwise equivalence (acceptance criterion 3):
-decomposed runs over 2/4 B200s (one process per GPU, torchrun) equal the
-single-rank run for every family and every mpi mode."""
+"""Multi-rank bitwise equivalence (acceptance criterion 3; the
+SPEC.md:702 matrix ranks {2,3,4,8} x modes): decomposed runs (one process
+per rank, torchrun) equal the single-rank run for every family and every
+mpi mode, bitwise.
+
+Ranks map to GPUs as ``LOCAL_RANK % device_count`` (dist.py).  On a box with
+fewer GPUs than ranks the ranks are OVERSUBSCRIBED onto the available
+devices: the control plane falls back to gloo (NCCL refuses two ranks on
+one device) and the halo data plane is unchanged -- CUDA IPC mappings of the
+neighbours' buffers and flags work between processes that share a device,
+and the device-side flag waits make progress because the driver time-slices
+the ranks' contexts.  So the CORE/OWNED split, the fused peer-store push of
+full mode, the copy-engine posts of basic/diagonal and the release/acquire
+flags all run on a 1-GPU box, just slower.
+"""
 import json
 import os
 import subprocess
@@ -12,65 +24,90 @@ torch = pytest.importorskip("torch")
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ALL = "acoustic,diffusion,damped,rotated,tti,elastic,elastic_col,visco"
 
 
-def _run(nproc, topo, shape, families, steps=10, timeout=900):
-    env = dict(os.environ, TOPO=topo, SHAPE=shape, FAMILIES=families, STEPS=str(steps))
+def _env(nproc, **extra):
+    env = dict(os.environ, **extra)
+    ndev = torch.cuda.device_count()
+    if nproc > ndev:
+        # time-sliced ranks wait longer for each other: a generous watchdog
+        env.setdefault("SDMP_TIMEOUT_MS", "240000")
+    return env
+
+
+def _torchrun(nproc, port, script, env, timeout):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", "--master-port=29517",
-           os.path.join(ROOT, "tests", "mp_worker.py")]
-    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.join(ROOT, *script)]
+    return subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+
+
+def _run(nproc, topo, shape, families, steps=10, timeout=1500, port=29517):
+    env = _env(nproc, TOPO=topo, SHAPE=shape, FAMILIES=families, STEPS=str(steps))
+    res = _torchrun(nproc, port, ("tests", "mp_worker.py"), env, timeout)
     out = res.stdout.strip().splitlines()
     rep = json.loads(out[-1]) if out and out[-1].startswith("{") else {}
     return res.returncode, rep, res.stderr[-4000:]
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
-                    reason="needs >= 2 GPUs")
+def _check(rc, rep, err, families):
+    assert rc == 0, (rep, err)
+    res = rep.get("results", {})
+    want = {f"{f}_{m}" for f in families.split(",") for m in ("basic", "diagonal", "full")}
+    assert set(res) == want, (sorted(res), sorted(want))
+    bad = {k: v for k, v in res.items() if not v["equal"]}
+    assert not bad, bad
+    # full mode kept the Listing-8 order on every rank (post -> CORE -> wait -> OWNED)
+    assert rep.get("order_ok", True), rep.get("order")
+
+
+needs_gpu = pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
+
+
+@needs_gpu
 @pytest.mark.parametrize("topo,shape", [("2,1,1", "40,36,32"), ("1,2,1", "36,40,32")])
-def test_two_gpus_all_families(topo, shape):
-    rc, rep, err = _run(2, topo, shape, "acoustic,diffusion,damped,rotated,tti,elastic,elastic_col,visco")
-    assert rc == 0, (rep, err)
-    assert rep["results"] and all(v["equal"] for v in rep["results"].values()), rep
+def test_two_ranks_all_families(topo, shape):
+    rc, rep, err = _run(2, topo, shape, ALL)
+    _check(rc, rep, err, ALL)
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 3,
-                    reason="needs >= 3 GPUs")
-def test_three_gpus_odd_rank_count():
+@needs_gpu
+def test_three_ranks_odd_rank_count():
     # SPEC acceptance matrix includes 3 ranks: uneven split along x
-    rc, rep, err = _run(3, "3,1,1", "50,36,32", "acoustic,damped,rotated,tti,elastic_col,visco")
-    assert rc == 0, (rep, err)
-    assert all(v["equal"] for v in rep["results"].values()), rep
+    fams = "acoustic,damped,rotated,tti,elastic_col,visco"
+    rc, rep, err = _run(3, "3,1,1", "50,36,32", fams, port=29521)
+    _check(rc, rep, err, fams)
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
-                    reason="needs >= 4 GPUs")
-def test_four_gpus_x_interior_ranks():
+@needs_gpu
+def test_four_ranks_x_interior_ranks():
     # (4,1,1): interior ranks with both x neighbours, as in the 8-GPU (4,2,1) layout
-    rc, rep, err = _run(4, "4,1,1", "64,36,32", "acoustic,diffusion,damped,rotated,tti,elastic,elastic_col,visco")
-    assert rc == 0, (rep, err)
-    assert all(v["equal"] for v in rep["results"].values()), rep
+    rc, rep, err = _run(4, "4,1,1", "64,36,32", ALL, port=29522)
+    _check(rc, rep, err, ALL)
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
-                    reason="needs >= 4 GPUs")
-def test_four_gpus_xy_split():
-    rc, rep, err = _run(4, "2,2,1", "44,40,32", "acoustic,diffusion,damped,rotated,tti,elastic,elastic_col,visco")
-    assert rc == 0, (rep, err)
-    assert all(v["equal"] for v in rep["results"].values()), rep
+@needs_gpu
+def test_four_ranks_xy_split():
+    rc, rep, err = _run(4, "2,2,1", "44,40,32", ALL, port=29523)
+    _check(rc, rep, err, ALL)
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
-                    reason="needs >= 4 GPUs")
+@needs_gpu
+def test_eight_ranks_4x2_layout():
+    """The BASELINE 8-GPU topology (4,2,1): interior ranks with x, y and
+    diagonal (xy-edge) neighbours -- up to 8 messages per rank per phase."""
+    rc, rep, err = _run(8, "4,2,1", "64,44,32", ALL, steps=8, timeout=2400, port=29524)
+    _check(rc, rep, err, ALL)
+
+
+@needs_gpu
 @pytest.mark.parametrize("nproc,mode", [(2, "basic"), (4, "full"), (4, "diagonal")])
-def test_listing4_2d_multi_gpu(nproc, mode):
+def test_listing4_2d_multi_rank(nproc, mode):
     """The paper's Listing 4 (2D diffusion, 4x4 grid) decomposed over 2 / 4
-    GPUs gives the printed values."""
-    env = dict(os.environ, STENCIL_DMP_MODE=mode)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", "--master-port=29518",
-           os.path.join(ROOT, "examples", "listing4_diffusion.py")]
-    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    ranks gives the printed values."""
+    env = _env(nproc, STENCIL_DMP_MODE=mode)
+    res = _torchrun(nproc, 29518, ("examples", "listing4_diffusion.py"), env, 900)
     assert res.returncode == 0, res.stderr[-3000:]
     out = res.stdout
     i = out.index("after 2 steps")
@@ -81,15 +118,12 @@ def test_listing4_2d_multi_gpu(nproc, mode):
     assert vals == want, out
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
-                    reason="needs >= 2 GPUs")
+@needs_gpu
 def test_halo_wait_watchdog():
     """A neighbour that never delivers its halo ends in a NativeError after
     SDMP_TIMEOUT_MS (device-side watchdog), not in a hang."""
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29519",
-           os.path.join(ROOT, "tests", "mp_watchdog.py")]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    env = dict(os.environ)
+    res = _torchrun(2, 29519, ("tests", "mp_watchdog.py"), env, 300)
     assert res.returncode == 0, res.stderr[-3000:]
     out = json.loads(res.stdout.strip().splitlines()[-1])
     assert out[0]["outcome"] == "timeout", out
