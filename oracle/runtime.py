@@ -41,8 +41,14 @@ class Rank:
 
 
 class Simulation:
-    def __init__(self, problem, shape, dims=None, mode="diagonal", messages=None):
+    def __init__(self, problem, shape, dims=None, mode="diagonal", messages=None, threads=1):
         self.p = problem
+        # threads > 1: each compute box is cut into x-slabs evaluated
+        # concurrently (numpy releases the GIL; every per-point update writes
+        # only its own box of an output buffer it does not read, so slabs are
+        # independent and the result is identical to one call)
+        self.threads = max(1, int(threads))
+        self._pool = None
         self.shape = tuple(shape)
         self.dims = tuple(dims) if dims else (1,) * len(shape)
         self.mode = mode
@@ -102,6 +108,20 @@ class Simulation:
                 dst = self.ranks[peer]
                 dst.buf(name, time, tsh)[_sl(rbox, dst.halo)] = data
 
+    def _compute(self, ph, rk, fb, time):
+        lo, hi = fb
+        n0 = hi[0] - lo[0]
+        if self.threads == 1 or n0 < 2 * self.threads:
+            ph.compute(rk, fb, time)
+            return
+        if self._pool is None:
+            from concurrent.futures import ThreadPoolExecutor
+            self._pool = ThreadPoolExecutor(self.threads)
+        cuts = np.linspace(lo[0], hi[0], self.threads + 1).astype(int)
+        boxes = [((int(a),) + tuple(lo[1:]), (int(b),) + tuple(hi[1:]))
+                 for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+        list(self._pool.map(lambda b: ph.compute(rk, b, time), boxes))
+
     # -- time loop ----------------------------------------------------------
     def run(self, time_m, time_M):
         for time in range(time_m, time_M + 1):
@@ -120,6 +140,6 @@ class Simulation:
                     for box in boxes:
                         if all(h > l for l, h in zip(*box)):
                             fb = tuple(tuple(x + h for x, h in zip(c, rk.halo)) for c in box)
-                            ph.compute(rk, fb, time)
+                            self._compute(ph, rk, fb, time)
                     if ph.after is not None:
                         ph.after(self, rk, time)

@@ -498,13 +498,293 @@ def recognise_var_star(eq: S.StencilEquation) -> Optional[VarStarKernel]:
     return VarStarKernel(u, statics, tuple(W for _ in range(nd)), eq, has_prev)
 
 
+class _Probe:
+    """Exact evaluation at seeded random rational values keyed by
+    (field spec, tshift, offsets) / symbol name, drawn on first use, so two
+    expressions over the same leaves see the same values.  ``rename`` maps
+    field specs of a template onto the fields a candidate role assignment
+    gives them (the template is built once and re-evaluated per assignment)."""
+
+    def __init__(self, seed):
+        self.rng = random.Random(seed)
+        self.vals = {}
+
+    def _value(self, key):
+        v = self.vals.get(key)
+        if v is None:
+            v = self.vals[key] = Fraction(self.rng.randint(1, 40), self.rng.randint(1, 12))
+        return v
+
+    def eval(self, expr, rename=None):
+        bind = {}
+        for n in _leaves(expr):
+            if isinstance(n, S.Symbol):
+                bind[n] = self._value(("symbol", n.name))
+            else:
+                spec = rename.get(n.spec, n.spec) if rename else n.spec
+                bind[n] = self._value((spec, n.tshift, n.offsets))
+        return S.eval_exact(expr, bind)
+
+
+def _matching_rename(eqs, templates, renames, samples=2):
+    """First rename under which every solved update in ``eqs`` equals its
+    template (same lhs after renaming) at ``samples`` independent exact
+    probes (the updates themselves are evaluated once per probe), or None."""
+    probes = [_Probe(1000 + seed) for seed in range(samples)]
+    cache = {}
+    for rename in renames:
+        ok = True
+        for si, pr in enumerate(probes):
+            for ei, (eq, tp) in enumerate(zip(eqs, templates)):
+                if rename.get(tp.lhs.spec, tp.lhs.spec) != eq.lhs.spec:
+                    ok = False
+                    break
+                if (si, ei) not in cache:
+                    cache[(si, ei)] = pr.eval(eq.rhs)
+                if cache[(si, ei)] != pr.eval(tp.rhs, rename):
+                    ok = False
+                    break
+            if not ok:
+                break
+        if ok:
+            return rename
+    return None
+
+
+def _solved_shape_ok(eq, time_order) -> bool:
+    u = eq.lhs.spec
+    return (not u.is_static and eq.lhs.tshift == 1 and not any(eq.lhs.offsets)
+            and not eq.temporaries and u.grid.ndims == 3 and u.time_order == time_order)
+
+
+def tti_updates(p: S.FieldSpec, r: S.FieldSpec, m: S.FieldSpec, epsp: S.FieldSpec,
+                delp: S.FieldSpec, a) -> Tuple[S.StencilEquation, S.StencilEquation]:
+    """The paper's two-field pseudo-acoustic TTI (Devito's
+    centred kernel form) written with the reference symbolics:
+
+        Gzz f = sum_i D_i(a_i sum_j a_j D_j f)   (nested centred first
+                derivatives, the reference's Deriv(coef * Deriv) lowering,
+                symbolics.py:556-566; radius = space order)
+        H0 f  = laplace f - Gzz f
+        m p.dt2 = epsp H0 p + delp Gzz r
+        m r.dt2 = delp H0 p + Gzz r
+
+    with epsp = 1 + 2 eps, delp = sqrt(1 + 2 delta) and the direction
+    cosines a = (sin t cos f, sin t sin f, cos t) as static fields, each
+    solved for the forward buffer by ``solve_forward`` (symbolics.py:629)."""
+    def gzz(f):
+        inner = S.add(*(S.mul(a[j].at(), f.d(j)) for j in range(3)))
+        return S.add(*(S.Deriv(S.mul(a[i].at(), inner), i, 1) for i in range(3)))
+
+    h0p = S.add(p.laplace, S.neg(gzz(p)))
+    gr = gzz(r)
+    eq_p = S.solve_forward(
+        S.Eq(S.mul(m.at(), p.dt2), S.add(S.mul(epsp.at(), h0p), S.mul(delp.at(), gr))),
+        p.forward)
+    eq_r = S.solve_forward(
+        S.Eq(S.mul(m.at(), r.dt2), S.add(S.mul(delp.at(), h0p), gr)), r.forward)
+    return eq_p, eq_r
+
+
+def recognise_tti(eq_p: S.StencilEquation, eq_r: S.StencilEquation) -> Optional[TTIKernel]:
+    """Match a pair of solved updates against ``tti_updates`` for some
+    assignment of their static fields to (m, epsp, delp, a_x, a_y, a_z):
+    epsp is the pointwise static only the p update reads, {m, delp} the
+    pointwise statics both read, the three statics read at offsets are the
+    direction cosines; the 2 x 6 remaining assignments are decided by exact
+    evaluation of one template (or None)."""
+    if not (_solved_shape_ok(eq_p, 2) and _solved_shape_ok(eq_r, 2)):
+        return None
+    p, r = eq_p.lhs.spec, eq_r.lhs.spec
+    if p == r or p.space_order != r.space_order or p.grid != r.grid:
+        return None
+    acc_p, acc_r = S.accesses(eq_p.rhs), S.accesses(eq_r.rhs)
+    for accs in (acc_p, acc_r):
+        if {a.spec for a in accs if not a.spec.is_static} != {p, r}:
+            return None
+
+    def split(accs):
+        st = {a.spec for a in accs if a.spec.is_static}
+        pw = {f for f in st if all(not any(a.offsets) for a in accs if a.spec == f)}
+        return pw, st - pw
+
+    pw_p, off_p = split(acc_p)
+    pw_r, off_r = split(acc_r)
+    if len(pw_p) != 3 or len(pw_r) != 2 or not pw_r < pw_p or off_p != off_r or len(off_p) != 3:
+        return None
+    epsp = next(iter(pw_p - pw_r))
+    import itertools
+    a0 = tuple(sorted(off_p, key=lambda f: f.name))
+    m0, d0 = sorted(pw_r, key=lambda f: f.name)
+    tp = tti_updates(p, r, m0, epsp, d0, a0)
+    renames = [{m0: m, d0: d, **dict(zip(a0, perm))}
+               for m, d in ((m0, d0), (d0, m0)) for perm in itertools.permutations(a0)]
+    rn = _matching_rename((eq_p, eq_r), tp, renames)
+    if rn is None:
+        return None
+    return TTIKernel(p, r, rn[m0], epsp, rn[d0], tuple(rn[f] for f in a0), p.space_order)
+
+
+# stress components in the order xx, yy, zz, xy, xz, yz
+_TAU_INDEX = {(0, 0): 0, (1, 1): 1, (2, 2): 2, (0, 1): 3, (0, 2): 4, (1, 2): 5}
+
+
+def _tau(i, j):
+    return _TAU_INDEX[(min(i, j), max(i, j))]
+
+
+def elastic_updates(v, tau, b: S.FieldSpec, lam: S.FieldSpec, mu: S.FieldSpec):
+    """The SPEC's collocated isotropic elastic system (SPEC.md:587-592;
+    PAPER.md:1041-1051 on one grid) written with the reference symbolics:
+
+        v_i.dt   = b sum_j D_j tau_ij
+        tau_ii.dt = lam sum_k D_k v_k[t+1] + 2 mu D_i v_i[t+1]
+        tau_ij.dt = mu (D_j v_i[t+1] + D_i v_j[t+1])     (i != j)
+
+    D = centred first derivative of the fields' space order; the stress
+    update reads the freshly updated velocity (``v.forward``).  Returns the
+    nine solved updates (3 velocity, then 6 stress)."""
+    out = []
+    for i in range(3):
+        div = S.add(*(tau[_tau(i, j)].d(j) for j in range(3)))
+        out.append(S.solve_forward(S.Eq(v[i].dt, S.mul(b.at(), div)), v[i].forward))
+
+    def dv(i, j):
+        return S.Deriv(v[i].forward, j, 1)
+
+    tr = S.add(*(dv(k, k) for k in range(3)))
+    for i in range(3):
+        rhs = S.add(S.mul(lam.at(), tr), S.mul(S.Const(Fraction(2)), mu.at(), dv(i, i)))
+        out.append(S.solve_forward(S.Eq(tau[i].dt, rhs), tau[i].forward))
+    for (i, j) in ((0, 1), (0, 2), (1, 2)):
+        k = _tau(i, j)
+        out.append(S.solve_forward(S.Eq(tau[k].dt, S.mul(mu.at(), S.add(dv(i, j), dv(j, i)))),
+                                   tau[k].forward))
+    return out
+
+
+def recognise_elastic(eqs: Sequence[S.StencilEquation]):
+    """Match nine solved first-order updates against ``elastic_updates``.
+
+    Roles are read off the access structure (velocity updates read stresses
+    at tshift 0 with offsets; a diagonal stress is read by one velocity
+    update along that velocity's axis, an off-diagonal one by two; b is the
+    static of the velocity updates; mu the only static of the shear-stress
+    updates, lam the other static of the normal-stress ones), then the whole
+    system is verified by exact evaluation.  Returns the velocity and stress
+    phases (collocated ``StaggeredPhase`` pair) or None."""
+    if len(eqs) != 9 or not all(_solved_shape_ok(e, 1) for e in eqs):
+        return None
+    lhs = [e.lhs.spec for e in eqs]
+    if len(set(lhs)) != 9 or len({f.space_order for f in lhs}) != 1:
+        return None
+    evolving = set(lhs)
+    vel, stress = [], []
+    for e in eqs:
+        ts = {a.tshift for a in S.accesses(e.rhs) if a.spec in evolving and a.spec != e.lhs.spec}
+        if ts == {0}:
+            vel.append(e)
+        elif ts == {1}:
+            stress.append(e)
+        else:
+            return None
+    if len(vel) != 3 or len(stress) != 6:
+        return None
+    vfields = [e.lhs.spec for e in vel]
+    tfields = {e.lhs.spec for e in stress}
+    readers = {f: [] for f in tfields}   # stress field -> [(velocity field, axes read along)]
+    for e in vel:
+        for f in tfields:
+            offs = [a.offsets for a in S.accesses(e.rhs) if a.spec == f]
+            if offs:
+                axes = {ax for o in offs for ax, k in enumerate(o) if k}
+                if len(axes) != 1:
+                    return None
+                readers[f].append((e.lhs.spec, axes.pop()))
+    v_of_axis, tau = {}, [None] * 6
+    for f, rd in readers.items():
+        if len(rd) == 1:
+            vf, ax = rd[0]
+            if ax in v_of_axis:
+                return None
+            v_of_axis[ax] = vf
+            tau[_tau(ax, ax)] = f
+    if sorted(v_of_axis) != [0, 1, 2]:
+        return None
+    axis_of_v = {vf: ax for ax, vf in v_of_axis.items()}
+    for f, rd in readers.items():
+        if len(rd) == 2:
+            (v1, a1), (v2, a2) = rd
+            i, j = axis_of_v[v1], axis_of_v[v2]
+            if {i, j} != {a1, a2} or i == j:
+                return None
+            tau[_tau(i, j)] = f
+    if any(t is None for t in tau):
+        return None
+    v = tuple(v_of_axis[a] for a in range(3))
+    statics = lambda e: {a.spec for a in S.accesses(e.rhs) if a.spec.is_static}
+    bs = set.union(*(statics(e) for e in vel))
+    shear = [e for e in stress if e.lhs.spec in tau[3:]]
+    normal = [e for e in stress if e.lhs.spec in tau[:3]]
+    mus = set.union(*(statics(e) for e in shear))
+    lams = set.union(*(statics(e) for e in normal)) - mus
+    if len(bs) != 1 or len(mus) != 1 or len(lams) != 1:
+        return None
+    b, mu, lam = bs.pop(), mus.pop(), lams.pop()
+    tp = elastic_updates(v, tau, b, lam, mu)
+    by_lhs = {e.lhs.spec: e for e in eqs}
+    if _matching_rename([by_lhs[t.lhs.spec] for t in tp], tp, [{}]) is None:
+        return None
+    so = v[0].space_order
+    kv = StaggeredPhase("v", v, tuple(tau), (b,), so=so, collocated=True)
+    kt = StaggeredPhase("t", v, tuple(tau), (lam, mu), so=so, collocated=True)
+    return kv, kt
+
+
+def _recognise_groups(pending: List[S.StencilEquation]):
+    """Multi-equation families among updates no single-equation family
+    matched: TTI pairs (each update reads the other's field) and the
+    nine-update collocated elastic system.  Returns [(first index, kernels,
+    consumed indices)]."""
+    out, used = [], set()
+    for i, e in enumerate(pending):
+        if i in used or not _solved_shape_ok(e, 2):
+            continue
+        others = {a.spec for a in S.accesses(e.rhs) if not a.spec.is_static} - {e.lhs.spec}
+        for j, f in enumerate(pending):
+            if j in used or j == i or f.lhs.spec not in others:
+                continue
+            # p is the update reading three pointwise statics (epsp, m, delp)
+            for a, b_ in ((e, f), (f, e)):
+                k = recognise_tti(a, b_)
+                if k is not None:
+                    out.append((min(i, j), [k], {i, j}))
+                    used |= {i, j}
+                    break
+            if i in used:
+                break
+    first_order = [i for i, e in enumerate(pending) if i not in used and _solved_shape_ok(e, 1)]
+    if len(first_order) >= 9:
+        ks = recognise_elastic([pending[i] for i in first_order[:9]])
+        if ks is not None:
+            out.append((first_order[0], list(ks), set(first_order[:9])))
+            used |= set(first_order[:9])
+    return out, used
+
+
 def recognise(equations: Sequence) -> List[object]:
-    """Solved updates -> kernel list (one kernel may own several updates)."""
-    kernels: List[object] = []
+    """Solved updates -> kernel list (one kernel may own several updates).
+
+    Single-update families first (star, damped star, rotated G_xx), then
+    the multi-update families among the rest (TTI pair, collocated elastic
+    system), placed at their first update's position.  Anything left
+    raises: there is no generic/CPU path."""
+    slots: List[object] = []     # kernels, or ("pending", index into pending)
+    pending: List[S.StencilEquation] = []
     seen = set()
     for eq in equations:
         if isinstance(eq, (StarKernel, VarStarKernel, RotatedKernel, TTIKernel, StaggeredPhase)):
-            kernels.append(eq)
+            slots.append(eq)
             continue
         if not isinstance(eq, S.StencilEquation):
             raise CompilerError(f"expected a solved update, got {type(eq).__name__}")
@@ -512,7 +792,7 @@ def recognise(equations: Sequence) -> List[object]:
         if fam is not None:
             if id(fam) not in seen:
                 seen.add(id(fam))
-                kernels.append(fam)
+                slots.append(fam)
             continue
         k = recognise_star(eq)
         if k is None:
@@ -520,12 +800,25 @@ def recognise(equations: Sequence) -> List[object]:
         if k is None:
             k = recognise_rotated(eq)
         if k is None:
-            raise CompilerError(
-                "equation not recognised as a supported kernel family (acoustic, "
-                "damped acoustic, diffusion, rotated G_xx, TTI, staggered "
-                "elastic/viscoelastic): "
-                + " ; ".join(S.format_equation(eq))[:300])
-        kernels.append(k)
+            slots.append(("pending", len(pending)))
+            pending.append(eq)
+        else:
+            slots.append(k)
+    groups, used = _recognise_groups(pending) if pending else ([], set())
+    left = [e for i, e in enumerate(pending) if i not in used]
+    if left:
+        raise CompilerError(
+            "equation not recognised as a supported kernel family (acoustic, "
+            "damped acoustic, diffusion, rotated G_xx, TTI pair, collocated "
+            "elastic system; staggered elastic/viscoelastic via kernels.py): "
+            + " ; ".join(S.format_equation(left[0]))[:300])
+    first = {g[0]: g[1] for g in groups}
+    kernels: List[object] = []
+    for sl in slots:
+        if isinstance(sl, tuple) and len(sl) == 2 and sl[0] == "pending":
+            kernels.extend(first.get(sl[1], []))
+        else:
+            kernels.append(sl)
     return kernels
 
 
@@ -826,12 +1119,17 @@ def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
             # buffer, which this phase's update does not write (explicit
             # scheme), so it runs on stream 1 beside the update, ordered
             # after everything stream 0 did before it (r03: C1 -4.5 us/step)
-            if my_interps:
+            # That holds only if the update never writes the sampled buffer
+            # (tshift 0) and the field has a separate buffer to write to;
+            # otherwise the interpolation runs on stream 0 first.
+            overlap = [t for t in my_interps
+                       if (t.field, 0) not in set(k.writes()) and t.field.time_buffers >= 2]
+            if overlap:
                 acts.append(Action("record", 0, event=ev))
                 acts.append(Action("streamwait", 1, event=ev))
                 ev += 1
             for t in my_interps:
-                acts.append(Action("interp", 1, sparse=t))
+                acts.append(Action("interp", 1 if t in overlap else 0, sparse=t))
             acts.append(Action("compute", 0, kernel=k, box=domain, region="DOMAIN"))
         elif mode == "basic":
             steps = basic_messages(decomp, rank, spot.radius)
@@ -875,6 +1173,12 @@ def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
             ev += 1
         for t in my_injects:
             acts.append(Action("inject", 0, sparse=t))
+    emitted = {id(a.sparse) for a in acts if a.kind in ("interp", "inject")}
+    for t in sparse_terms:
+        if id(t) not in emitted:
+            what = "reads" if t.kind == "interp" else "writes"
+            raise CompilerError(f"{t.kind} of {t.sparse.name!r} on field {t.field.name!r}: no "
+                                f"kernel of this Operator {what} that field")
     if ev > 32:
         raise CompilerError("too many stream joins per step")
     if not exchange:

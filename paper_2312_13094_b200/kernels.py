@@ -223,11 +223,13 @@ def tti_model(grid: Grid, so: int = 8, vp=None) -> KernelDef:
     _fill(([m] if vp is None else []) + [epsp, delp] + a, law)
     if vp is not None:
         _set_domain(m, (1.0 / vp ** 2).float())
-    k = CP.TTIKernel(p.spec, r.spec, m.spec, epsp.spec, delp.spec,
-                     (a[0].spec, a[1].spec, a[2].spec), so)
+    # the system as update equations (reference symbolics); the Operator
+    # recognises the pair as the TTI family (compiler.recognise_tti)
+    eqs = list(CP.tti_updates(p.spec, r.spec, m.spec, epsp.spec, delp.spec,
+                              tuple(f.spec for f in a)))
     fields = {"p": p, "r": r, "m": m, "epsp": epsp, "delp": delp, "ax": a[0], "ay": a[1],
               "az": a[2]}
-    return KernelDef("tti", fields, [k], bytes_per_point=48, working_set=12)
+    return KernelDef("tti", fields, [], eqs, bytes_per_point=48, working_set=12)
 
 
 def rotated_model(grid: Grid, so: int = 8, vp=None, name: str = "u") -> KernelDef:
@@ -294,14 +296,23 @@ def elastic_model(grid: Grid, so: int = 8, collocated: bool = False) -> KernelDe
         return 1.0 / rho, rho * (vp ** 2 - 2.0 * vs ** 2), rho * vs ** 2
 
     _fill([b, lam, mu], law)
-    kv = CP.StaggeredPhase("v", tuple(f.spec for f in v), tuple(f.spec for f in t),
-                           (b.spec,), so=so, collocated=collocated)
-    kt = CP.StaggeredPhase("t", tuple(f.spec for f in v), tuple(f.spec for f in t),
-                           (lam.spec, mu.spec), so=so, collocated=collocated)
     fields = {f.name: f for f in v + t}
     fields.update({"b": b, "lam": lam, "mu": mu})
-    return KernelDef("elastic_collocated" if collocated else "elastic", fields, [kv, kt],
-                     bytes_per_point=120, working_set=21)
+    if collocated:
+        # the SPEC's elastic_kernel as nine update equations (reference
+        # symbolics); recognised as the collocated pair of phases
+        # (compiler.recognise_elastic)
+        eqs = CP.elastic_updates(tuple(f.spec for f in v), tuple(f.spec for f in t),
+                                 b.spec, lam.spec, mu.spec)
+        return KernelDef("elastic_collocated", fields, [], eqs, bytes_per_point=120,
+                         working_set=21)
+    # staggered (Virieux) offsets are half-integer: not expressible in the
+    # reference symbolics (integer offsets) -> kernel descriptors
+    kv = CP.StaggeredPhase("v", tuple(f.spec for f in v), tuple(f.spec for f in t),
+                           (b.spec,), so=so)
+    kt = CP.StaggeredPhase("t", tuple(f.spec for f in v), tuple(f.spec for f in t),
+                           (lam.spec, mu.spec), so=so)
+    return KernelDef("elastic", fields, [kv, kt], bytes_per_point=120, working_set=21)
 
 
 def viscoelastic_model(grid: Grid, so: int = 16, qp: float = 100.0, qs: float = 50.0,

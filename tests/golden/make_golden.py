@@ -43,6 +43,45 @@ def case_equations(S, kind, ndims, so):
         inner = S.add(*(S.mul(a[j].at(), u.d(j)) for j in range(3)))
         gxx = S.add(*(S.Deriv(S.mul(a[i].at(), inner), i, 1) for i in range(3)))
         return S.Eq(m.at() * u.dt2 - gxx), u.forward
+    if kind in ("tti_p", "tti_r"):
+        # the paper's two-field TTI (the same construction
+        # as compiler.tti_updates): Gzz f = sum_i D_i(a_i sum_j a_j D_j f),
+        # H0 = laplace - Gzz, m p.dt2 = epsp H0 p + delp Gzz r,
+        # m r.dt2 = delp H0 p + Gzz r
+        F = lambda n, to: S.FieldSpec(name=n, grid=g, space_order=so, time_order=to)
+        p, r, m, epsp, delp = F("p", 2), F("r", 2), F("m", 0), F("epsp", 0), F("delp", 0)
+        a = [F(f"a{S.AXIS_NAMES[i]}", 0) for i in range(3)]
+
+        def gzz(f):
+            inner = S.add(*(S.mul(a[j].at(), f.d(j)) for j in range(3)))
+            return S.add(*(S.Deriv(S.mul(a[i].at(), inner), i, 1) for i in range(3)))
+
+        h0p = S.add(p.laplace, S.neg(gzz(p)))
+        gr = gzz(r)
+        if kind == "tti_p":
+            return (S.Eq(S.mul(m.at(), p.dt2), S.add(S.mul(epsp.at(), h0p), S.mul(delp.at(), gr))),
+                    p.forward)
+        return S.Eq(S.mul(m.at(), r.dt2), S.add(S.mul(delp.at(), h0p), gr)), r.forward
+    if kind.startswith("elastic_"):
+        # the SPEC's collocated elastic_kernel (the same
+        # construction as compiler.elastic_updates): one velocity, one normal
+        # and one shear stress update
+        F = lambda n, to: S.FieldSpec(name=n, grid=g, space_order=so, time_order=to)
+        v = [F(n, 1) for n in ("vx", "vy", "vz")]
+        t = [F(n, 1) for n in ("txx", "tyy", "tzz", "txy", "txz", "tyz")]
+        b, lam, mu = F("b", 0), F("lam", 0), F("mu", 0)
+        T = {(0, 0): 0, (1, 1): 1, (2, 2): 2, (0, 1): 3, (0, 2): 4, (1, 2): 5}
+        tau = lambda i, j: t[T[(min(i, j), max(i, j))]]
+        dv = lambda i, j: S.Deriv(v[i].forward, j, 1)
+        if kind == "elastic_vx":
+            div = S.add(*(tau(0, j).d(j) for j in range(3)))
+            return S.Eq(v[0].dt, S.mul(b.at(), div)), v[0].forward
+        if kind == "elastic_txx":
+            tr = S.add(*(dv(k, k) for k in range(3)))
+            rhs = S.add(S.mul(lam.at(), tr), S.mul(S.Const(Fraction(2)), mu.at(), dv(0, 0)))
+            return S.Eq(t[0].dt, rhs), t[0].forward
+        if kind == "elastic_txy":
+            return S.Eq(t[3].dt, S.mul(mu.at(), S.add(dv(0, 1), dv(1, 0)))), t[3].forward
     raise ValueError(kind)
 
 
@@ -51,6 +90,8 @@ CASES = (
     + [("diffusion", 3, so) for so in (2, 4)]
     + [("acoustic", nd, so) for nd in (2, 3) for so in (2, 4, 8, 12, 16)]
     + [("tti_gxx", 3, so) for so in (2, 4, 8)]
+    + [(k, 3, so) for k in ("tti_p", "tti_r") for so in (4, 8)]
+    + [(k, 3, so) for k in ("elastic_vx", "elastic_txx", "elastic_txy") for so in (4, 8, 16)]
 )
 
 

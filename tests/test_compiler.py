@@ -242,3 +242,109 @@ def test_recognise_rotated_gxx_golden_form():
     bad = S.add(*(S.Deriv(S.mul(a[i].at(), bad_inner), i, 1) for i in range(3)))
     with pytest.raises(CP.CompilerError):
         CP.recognise([S.solve_forward(S.Eq(m.at() * u.dt2 - bad), u.forward)])
+
+
+# --- multi-update families written as equations -----------------------------
+
+def _tti_fields(so, n=16):
+    g = S.GridSpec((n,) * 3, (10.0 * (n - 1),) * 3)
+    F = lambda name, to: S.FieldSpec(name, g, so, to)
+    return (F("p", 2), F("r", 2), F("m", 0), F("epsp", 0), F("delp", 0),
+            [F("ax", 0), F("ay", 0), F("az", 0)])
+
+
+@pytest.mark.parametrize("so", [4, 8])
+def test_recognise_tti_pair_from_equations(so):
+    """The paper's two-field TTI written as Eqs is
+    recognised as ONE TTI kernel whatever the equation order, and the roles
+    of its static fields come out of the exact probe, not their names."""
+    p, r, m, e, d, a = _tti_fields(so)
+    eq_p, eq_r = CP.tti_updates(p, r, m, e, d, a)
+    for eqs in ([eq_p, eq_r], [eq_r, eq_p]):
+        ks = CP.recognise(eqs)
+        assert len(ks) == 1 and isinstance(ks[0], CP.TTIKernel)
+        k = ks[0]
+        assert (k.p, k.r, k.m, k.epsp, k.delp, k.a, k.so) == (p, r, m, e, d, tuple(a), so)
+    # the same system with m and delp (and two direction cosines) swapped
+    eq_p2, eq_r2 = CP.tti_updates(p, r, d, e, m, [a[2], a[1], a[0]])
+    k = CP.recognise([eq_p2, eq_r2])[0]
+    assert (k.m, k.delp, k.a) == (d, m, (a[2], a[1], a[0]))
+    # a user-written equivalent form: p.dt2 = (...)/m, solved by the reference solver
+    gzz = lambda f: S.add(*(S.Deriv(S.mul(a[i].at(), S.add(*(S.mul(a[j].at(), f.d(j))
+                                                                for j in range(3)))), i, 1)
+                            for i in range(3)))
+    h0 = p.laplace - gzz(p)
+    user_p = S.solve_forward(S.Eq(p.dt2, (e.at() * h0 + d.at() * gzz(r)) / m.at()), p.forward)
+    user_r = S.solve_forward(S.Eq(r.dt2, (d.at() * h0 + gzz(r)) / m.at()), r.forward)
+    assert isinstance(CP.recognise([user_r, user_p])[0], CP.TTIKernel)
+
+
+def test_tti_wrong_physics_rejected():
+    p, r, m, e, d, a = _tti_fields(4)
+    gzz = lambda f: S.add(*(S.Deriv(S.mul(a[i].at(), S.add(*(S.mul(a[j].at(), f.d(j))
+                                                                for j in range(3)))), i, 1)
+                            for i in range(3)))
+    h0 = p.laplace - gzz(p)
+    # sign flip on the coupling term: not the TTI system
+    bad_p = S.solve_forward(S.Eq(m.at() * p.dt2, e.at() * h0 - d.at() * gzz(r)), p.forward)
+    good_r = CP.tti_updates(p, r, m, e, d, a)[1]
+    with pytest.raises(CP.CompilerError, match="not recognised"):
+        CP.recognise([bad_p, good_r])
+
+
+def _elastic_fields(so, n=16):
+    g = S.GridSpec((n,) * 3, (10.0 * (n - 1),) * 3)
+    F = lambda name, to: S.FieldSpec(name, g, so, to)
+    v = [F(x, 1) for x in ("vx", "vy", "vz")]
+    t = [F(x, 1) for x in ("txx", "tyy", "tzz", "txy", "txz", "tyz")]
+    return v, t, F("b", 0), F("lam", 0), F("mu", 0)
+
+
+@pytest.mark.parametrize("so", [4, 8, 16])
+def test_recognise_collocated_elastic_from_equations(so):
+    """The SPEC's elastic_kernel as nine Eqs -> the
+    velocity and stress phases, in that order, with roles read off the
+    access structure (field names are irrelevant)."""
+    v, t, b, lam, mu = _elastic_fields(so)
+    eqs = CP.elastic_updates(v, t, b, lam, mu)
+    import random
+    random.Random(so).shuffle(eqs)
+    kv, kt = CP.recognise(eqs)
+    assert (kv.kind, kt.kind) == ("v", "t") and kv.collocated and kt.collocated
+    assert kv.v == tuple(v) and kv.tau == tuple(t) and kv.params == (b,)
+    assert kt.params == (lam, mu) and kv.so == so
+    # relabelled: components given in another order still map to their roles
+    v2 = [v[1], v[2], v[0]]
+    t2 = [t[1], t[2], t[0], t[5], t[3], t[4]]  # yy,zz,xx,(yz as xy)...
+    eqs2 = CP.elastic_updates(v2, t2, b, lam, mu)
+    kv2, kt2 = CP.recognise(eqs2)
+    assert kv2.v == tuple(v2) and kv2.tau == tuple(t2)
+
+
+def test_elastic_wrong_physics_rejected():
+    v, t, b, lam, mu = _elastic_fields(4)
+    eqs = CP.elastic_updates(v, t, b, lam, mu)
+    # txy with a factor 2 on the shear strain: not the elastic system
+    dv = lambda i, j: S.Deriv(v[i].forward, j, 1)
+    bad = S.solve_forward(S.Eq(t[3].dt, S.mul(S.Const(Fraction(2)), mu.at(),
+                                               S.add(dv(0, 1), dv(1, 0)))), t[3].forward)
+    eqs = [bad if e.lhs.spec == t[3] else e for e in eqs]
+    with pytest.raises(CP.CompilerError, match="not recognised"):
+        CP.recognise(eqs)
+
+
+def test_sparse_term_on_unused_field_raises():
+    """A receiver on a field no kernel of the Operator reads (or a source
+    into a field none writes) is an error, not a silently empty trace."""
+    from paper_2312_13094_b200 import api
+    grid = api.Grid((12, 12, 12), (110.0,) * 3, comm="self")
+    u = api.TimeFunction("u_sp", grid, space_order=4, time_order=2)
+    m = api.Function("m_sp", grid, space_order=4)
+    w = api.TimeFunction("w_sp", grid, space_order=4, time_order=2)
+    eq = S.solve_forward(S.Eq(m.at() * u.dt2 - u.laplace), u.forward)
+    rec = api.SparseTimeFunction("rec_sp", grid, 2, 4, coordinates=[(10.0,) * 3, (20.0,) * 3])
+    op = api.Operator([eq, rec.interpolate(w)])
+    with pytest.raises(CP.CompilerError, match="no kernel"):
+        op.plan("diagonal")
+    op2 = api.Operator([eq, rec.interpolate(u)])
+    assert any(a.kind == "interp" for a in op2.plan("diagonal").actions)

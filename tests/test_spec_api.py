@@ -4,6 +4,7 @@ kernel factories."""
 import numpy as np
 import pytest
 
+from paper_2312_13094_b200 import kernels as KD
 from paper_2312_13094_b200 import api
 from paper_2312_13094_b200 import compiler as CP
 from paper_2312_13094_b200 import decomposition as DC
@@ -56,7 +57,12 @@ def test_kernel_factories_build_the_named_families():
     ks = CP.recognise([api._as_update(q) for q in SP.tti_gxx_kernel(grid, so=4, name="w").equations])
     assert isinstance(ks[0], CP.RotatedKernel)
     el = SP.elastic_kernel(grid, so=4)
-    assert all(k.collocated for k in el.kernels)
+    assert el.kernels == [] and len(el.equations) == 9   # written as update equations
+    kv, kt = CP.recognise([api._as_update(q) for q in el.equations])
+    assert kv.collocated and kt.collocated and (kv.kind, kt.kind) == ("v", "t")
+    tti = KD.tti_model(grid, so=4)
+    assert tti.kernels == [] and len(tti.equations) == 2
+    assert isinstance(CP.recognise(tti.equations)[0], CP.TTIKernel)
     ac = SP.acoustic_kernel(grid, so=4, name="ua")
     assert isinstance(CP.recognise([api._as_update(q) for q in ac.equations])[0], CP.StarKernel)
 

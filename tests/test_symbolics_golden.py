@@ -59,3 +59,38 @@ def test_pow_extension():
     assert S.DT ** 2 == S.mul(S.DT, S.DT)
     with pytest.raises(TypeError):
         S.DT ** 0.5
+
+
+def _case(kind, so):
+    return next(c for c in GOLD["cases"] if (c["kind"], c["so"]) == (kind, so))
+
+
+@pytest.mark.parametrize("so", [4, 8])
+def test_tti_family_template_is_the_reference_discretization(so):
+    """compiler.tti_updates (the template the Operator recognises TTI by)
+    prints exactly the solved updates the REFERENCE symbolics produce for
+    the paper's two-field TTI system (golden from make_golden.py)."""
+    import hashlib
+    from paper_2312_13094_b200 import compiler as CP
+    g = S.GridSpec(shape=(16,) * 3, extent=(2.0,) * 3)
+    F = lambda n, to: S.FieldSpec(name=n, grid=g, space_order=so, time_order=to)
+    eq_p, eq_r = CP.tti_updates(F("p", 2), F("r", 2), F("m", 0), F("epsp", 0), F("delp", 0),
+                                [F(f"a{c}", 0) for c in "xyz"])
+    for eq, kind in ((eq_p, "tti_p"), (eq_r, "tti_r")):
+        text = "\n".join(S.format_equation(eq))
+        assert hashlib.sha256(text.encode()).hexdigest() == _case(kind, so)["sha256"], kind
+
+
+@pytest.mark.parametrize("so", [4, 8, 16])
+def test_collocated_elastic_template_is_the_reference_discretization(so):
+    import hashlib
+    from paper_2312_13094_b200 import compiler as CP
+    g = S.GridSpec(shape=(16,) * 3, extent=(2.0,) * 3)
+    F = lambda n, to: S.FieldSpec(name=n, grid=g, space_order=so, time_order=to)
+    v = [F(n, 1) for n in ("vx", "vy", "vz")]
+    t = [F(n, 1) for n in ("txx", "tyy", "tzz", "txy", "txz", "tyz")]
+    eqs = CP.elastic_updates(v, t, F("b", 0), F("lam", 0), F("mu", 0))
+    by = {e.lhs.spec.name: e for e in eqs}
+    for name, kind in (("vx", "elastic_vx"), ("txx", "elastic_txx"), ("txy", "elastic_txy")):
+        text = "\n".join(S.format_equation(by[name]))
+        assert hashlib.sha256(text.encode()).hexdigest() == _case(kind, so)["sha256"], kind
