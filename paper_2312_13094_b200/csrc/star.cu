@@ -14,12 +14,12 @@
 //
 //  * star_generic: one thread per point, taps through L1/L2.  Any radius,
 //    any alignment, 2D (radius_z = 0) included.  Used for thin OWNED slabs.
-//  * star_stream<R>: HBM-roofline kernel.  A CTA owns a 128(z) x 16(y) tile
-//    and streams along x (slowest axis).  Each thread keeps a float4 x-window
-//    of 2R+1 planes in registers; the centre plane (tile + R halo in y and z)
-//    is staged in shared memory for the y/z taps.  u0 is read from DRAM once
-//    (halo re-reads of neighbouring tiles hit L2), u2 and m are streamed
-//    once (evict-first), u1 written once: 16 B / point.
+//  * star_tma<R,TY> / star_tma2<R,TY>: HBM-roofline kernels.  A CTA owns a
+//    128(z) x TY(y) tile and streams along x (slowest axis); a producer warp
+//    stages plane tiles with TMA, each consumer thread keeps a float4
+//    x-window of 2R+1 planes in registers and reads y/z taps from the staged
+//    centre plane.  u0 is read from DRAM once (halo re-reads of neighbouring
+//    tiles hit L2), u2 and m streamed once, u1 written once: 16 B / point.
 #include <cstdlib>
 
 #include "common.cuh"
@@ -103,155 +103,18 @@ __global__ void __launch_bounds__(256) star_generic(StarParams p, const Push pus
 }
 
 // ---------------------------------------------------------------------------
-// streaming: register x-window + shared y/z plane
+// streaming kernels: tile width along z
 
 constexpr int kTZ = 128;  // z points per tile (32 lanes x float4)
-constexpr int kTY = 16;   // y rows per tile (one warp per row)
 
 __host__ __device__ constexpr int round4(int r) { return (r + 3) & ~3; }
 
-template <int R>
-struct StreamSmem {
-  static constexpr int OFF = round4(R);           // left pad keeps float4 alignment
-  static constexpr int PITCH = OFF + kTZ + OFF;   // floats per smem row
-  static constexpr int ROWS = kTY + 2 * R;
-  static constexpr int BYTES = PITCH * ROWS * 4;
-};
-
-__device__ __forceinline__ float4 ld4(const float* p) {
-  return __ldg(reinterpret_cast<const float4*>(p));
-}
-__device__ __forceinline__ float4 ld4_stream(const float* p) {
-  return __ldcs(reinterpret_cast<const float4*>(p));
-}
 // lanes (x, y) or (z, w) of a float4 as one packed pair
 __device__ __forceinline__ V2 f4pair(const float4& v, int h) {
   return h == 0 ? v2pack(v.x, v.y) : v2pack(v.z, v.w);
 }
 __device__ __forceinline__ float f4get(const float4& v, int j) {
   return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
-}
-
-template <int R>
-__global__ void __launch_bounds__(kTZ / 4 * kTY, 1)
-star_stream(StarParams p, int xchunk) {
-  using S = StreamSmem<R>;
-  extern __shared__ __align__(16) float sm[];
-  const int tz = threadIdx.x, ty = threadIdx.y;
-  const int z0 = p.g.lo[2] + blockIdx.x * kTZ;
-  const int y0 = p.g.lo[1] + blockIdx.y * kTY;
-  const int xa = p.g.lo[0] + blockIdx.z * xchunk;
-  const int xb = min(xa + xchunk, p.g.hi[0]);
-  const int z = z0 + 4 * tz, y = y0 + ty;
-  const int64_t sx = p.g.sx, sy = p.g.sy;
-  // keep a window if this column feeds an active point's y/z taps
-  const bool feeds = (z < p.g.hi[2] + R) && (y < p.g.hi[1] + R);
-  const bool active = (z < p.g.hi[2]) && (y < p.g.hi[1]);
-  const float* __restrict__ u0 = p.u0;
-  const int64_t col = (int64_t)y * sy + z;
-
-  float4 w[2 * R + 1];
-  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-  for (int k = 0; k < 2 * R; ++k)
-    w[k] = feeds ? ld4(u0 + (int64_t)(xa - R + k) * sx + col) : zero4;
-
-  // y-halo loaders: 2R rows x 32 float4
-  const int li = ty * 32 + tz;
-  const bool yh_load = li < 2 * R * 32;
-  const int yh_row = li / 32;                                  // 0..2R-1
-  const int yh_srow = yh_row < R ? yh_row : yh_row + kTY;      // smem row
-  const int yh_gy = y0 - R + yh_srow;
-  const int yh_z = z0 + 4 * (li % 32);
-  const bool yh_ok = yh_load && yh_gy < p.g.hi[1] + R && yh_z < p.g.hi[2] + R;
-  // z-halo loaders: kTY rows x 2R scalars
-  const bool zh_load = li < kTY * 2 * R;
-  const int zh_row = li / (2 * R);
-  const int zh_c = li % (2 * R);
-  const int zh_gz = zh_c < R ? z0 - R + zh_c : z0 + kTZ + (zh_c - R);
-  const int zh_scol = zh_c < R ? S::OFF - R + zh_c : S::OFF + kTZ + (zh_c - R);
-  const int zh_gy = y0 + zh_row;
-  const bool zh_ok = zh_load && zh_gy < p.g.hi[1] + R && zh_gz < p.g.hi[2] + R;
-
-  float* my_row = sm + (ty + R) * S::PITCH + S::OFF + 4 * tz;
-
-  for (int x = xa; x < xb; ++x) {
-    const int64_t px = (int64_t)x * sx;
-    if (feeds) w[2 * R] = ld4(u0 + px + R * sx + col);
-    float4 u2v = zero4, mv = make_float4(1.f, 1.f, 1.f, 1.f);
-    if (active) {
-      if (p.u2) u2v = ld4_stream(p.u2 + px + col);
-      if (p.m) mv = ld4_stream(p.m + px + col);
-    }
-    float4 yh = zero4;
-    if (yh_ok) yh = ld4(u0 + px + (int64_t)yh_gy * sy + yh_z);
-    float zh = 0.f;
-    if (zh_ok) zh = __ldg(u0 + px + (int64_t)zh_gy * sy + zh_gz);
-
-    *reinterpret_cast<float4*>(my_row) = w[R];
-    if (yh_load) *reinterpret_cast<float4*>(sm + yh_srow * S::PITCH + S::OFF + 4 * (li % 32)) = yh;
-    if (zh_load) sm[(zh_row + R) * S::PITCH + zh_scol] = zh;
-    __syncthreads();
-
-    if (active) {
-      // z window: positions z-OFF .. z+3+OFF as float4s
-      constexpr int NZW = (4 + 2 * S::OFF) / 4;
-      float zw[4 * NZW];
-#pragma unroll
-      for (int q = 0; q < NZW; ++q) {
-        float4 v = *reinterpret_cast<const float4*>(my_row - S::OFF + 4 * q);
-        zw[4 * q + 0] = v.x; zw[4 * q + 1] = v.y; zw[4 * q + 2] = v.z; zw[4 * q + 3] = v.w;
-      }
-      float4 yt_m[R], yt_p[R];
-#pragma unroll
-      for (int k = 1; k <= R; ++k) {
-        yt_m[k - 1] = *reinterpret_cast<const float4*>(my_row - k * S::PITCH);
-        yt_p[k - 1] = *reinterpret_cast<const float4*>(my_row + k * S::PITCH);
-      }
-      float out[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        auto xs = [&](int k) { return __fadd_rn(f4get(w[R - k], j), f4get(w[R + k], j)); };
-        auto ys = [&](int k) { return __fadd_rn(f4get(yt_m[k - 1], j), f4get(yt_p[k - 1], j)); };
-        auto zs = [&](int k) { return __fadd_rn(zw[S::OFF + j - k], zw[S::OFF + j + k]); };
-        out[j] = star_point<R, R, R>(p, f4get(w[R], j), f4get(u2v, j), f4get(mv, j),
-                                     R, R, R, xs, ys, zs, p.A, p.B);
-      }
-      __stcs(reinterpret_cast<float4*>(p.u1 + px + col),
-             make_float4(out[0], out[1], out[2], out[3]));
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 2 * R; ++k) w[k] = w[k + 1];
-  }
-}
-
-template <int R>
-static int launch_stream(const StarParams& p, cudaStream_t st) {
-  using S = StreamSmem<R>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    SDMP_CUDA(cudaFuncSetAttribute(star_stream<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   S::BYTES));
-    attr_set = true;
-  }
-  const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
-  dim3 block(kTZ / 4, kTY);
-  const int tz = (nz + kTZ - 1) / kTZ, ty = (ny + kTY - 1) / kTY;
-  // ~4 CTAs per SM in total, but keep x chunks >= 8R planes so the
-  // window priming (2R planes) stays a small overhead.
-  const int64_t tiles = (int64_t)tz * ty;
-  int64_t want = (4ll * num_sms() + tiles - 1) / tiles;
-  int64_t maxchunks = nx / (8 * R) > 0 ? nx / (8 * R) : 1;
-  int nch = (int)(want < maxchunks ? want : maxchunks);
-  if (nch < 1) nch = 1;
-  if (nch > 65535) nch = 65535;
-  const int chunk = (nx + nch - 1) / nch;
-  nch = (nx + chunk - 1) / chunk;
-  dim3 grid(tz, ty, nch);
-  star_stream<R><<<grid, block, S::BYTES, st>>>(p, chunk);
-  SDMP_LAUNCHED();
-  return SDMP_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -353,19 +216,17 @@ struct TmaCfg {
 
 // x-window as an unrolled register ring (no per-plane register moves) for
 // the wide stencils; SDMP_STAR_RING_MIN sets the smallest radius using it
-#ifndef SDMP_STAR_RING_MIN
-#define SDMP_STAR_RING_MIN 1
-#endif
-#ifndef SDMP_TMA2_TY8
-#define SDMP_TMA2_TY8 14  // rows per CTA of star_tma2<8> (A/B)
-#endif
-#ifndef SDMP_TMA2_UNROLL
-#define SDMP_TMA2_UNROLL 2
-#endif
-constexpr int kTma2Unroll = SDMP_TMA2_UNROLL;
+// the x-window of star_tma is an unrolled register ring up to R = 4 (r02
+// A/B: wider stencils lose to code size); star_tma2 unrolls its x-windows
+// by two planes (r03 A/B) and runs 14-row tiles at R = 8 (8 warps, 208
+// registers; 12 and 16 rows measured slower).  (r04 A/B, dropped: one
+// accumulation chain per axis instead of one per point -- SO-16 unchanged,
+// SO-12 -2%, the damped SO-16 stream op -25%.)
+constexpr int kTma2Unroll = 2;
+constexpr int kTma2RowsR8 = 14;
 
 template <int R>
-constexpr bool kStarRing = R >= SDMP_STAR_RING_MIN && R <= 4;  // r02 A/B: wide stencils lose
+constexpr bool kStarRing = R >= 1 && R <= 4;
 
 template <int R, int TY>
 __global__ void __launch_bounds__(TmaCfg<R, TY>::THREADS, 1)
@@ -556,7 +417,6 @@ static int launch_tma(const StarParams& p, cudaStream_t st, const int64_t full[3
   const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
   const int tz = (nz + kTZ - 1) / kTZ, ty = (ny + TY - 1) / TY;
   int nch = pick_chunks((int64_t)tz * ty, nx, R, ctas, 4.0);
-  if (const char* e = getenv("SDMP_STAR_NCH")) nch = std::max(1, std::min(nx, atoi(e)));  // A/B
   const int chunk = (nx + nch - 1) / nch;
   nch = (nx + chunk - 1) / chunk;
   SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");
@@ -632,7 +492,7 @@ star_tma2(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ 
   constexpr int W = 2 * R + 1;
   // x-windows unrolled by U planes: plane slots are constants inside the
   // unrolled group and the 2R live planes move down once per group (2R / U
-  // register moves per plane instead of 2R; r03 A/B, SDMP_TMA2_UNROLL)
+  // register moves per plane instead of 2R; r03 A/B)
   constexpr int U = kTma2Unroll;
   float4 w0[W + U - 1], w1[W + U - 1];
 #pragma unroll
@@ -836,7 +696,7 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
   p.u0 = u0; p.u2 = (B == 0.0f) ? nullptr : u2; p.m = m; p.u1 = u1;
   p.m_is_scale = (variant & SDMP_VARIANT_M_IS_SCALE) ? 1 : 0;
   variant &= 0xff;
-  if (variant == 0) {  // SDMP_STAR_VARIANT: development A/B of the launch shapes
+  if (variant == 0) {  // SDMP_STAR_VARIANT (tests): 1 generic, 3 one-row TMA at every R
     const char* e = getenv("SDMP_STAR_VARIANT");
     variant = e ? atoi(e) : 0;
   }
@@ -857,38 +717,14 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
                           (((uintptr_t)u0 | (uintptr_t)u1 | (uintptr_t)u2 | (uintptr_t)m) % 16 == 0);
   // unaligned / unequal-radius boxes always take the generic kernel
   if (variant == 1 || !streamable) return launch_generic(p, st, push);
-  if (variant == 2 && push.ndir == 0) {  // baseline kernel: no fused push
-    switch (R) {
-      case 1: return launch_stream<1>(p, st);
-      case 2: return launch_stream<2>(p, st);
-      case 3: return launch_stream<3>(p, st);
-      case 4: return launch_stream<4>(p, st);
-      case 5: return launch_stream<5>(p, st);
-      case 6: return launch_stream<6>(p, st);
-      case 7: return launch_stream<7>(p, st);
-      case 8: return launch_stream<8>(p, st);
-    }
-  }
   // wide stencils: two rows per thread.  16-row tiles (9 warps: ptxas caps
   // registers at 168) while the two x-windows fit; R = 8 needs ~210
-  // registers, so 12 / 14-row tiles (<= 8 warps, 255 registers)
-  if (variant == 0 || variant == 6) {
+  // registers, so 14-row tiles (8 warps, 255 registers)
+  if (variant == 0) {
     switch (R) {
       case 6: return launch_tma2<6, 16>(p, st, full, push);
       case 7: return launch_tma2<7, 16>(p, st, full, push);
-      case 8: return launch_tma2<8, SDMP_TMA2_TY8>(p, st, full, push);
-    }
-  }
-  if (variant == 8) {  // A/B: 8-row tiles, two CTAs per SM (small grids)
-    switch (R) {
-      case 2: return launch_tma<2, 8>(p, st, full, push, 2);
-      case 4: return launch_tma<4, 8>(p, st, full, push, 2);
-    }
-  }
-  if (variant == 7) {  // A/B
-    switch (R) {
-      case 7: return launch_tma2<7, 14>(p, st, full, push);
-      case 8: return launch_tma2<8, 12>(p, st, full, push);
+      case 8: return launch_tma2<8, kTma2RowsR8>(p, st, full, push);
     }
   }
   switch (R) {  // variant 0 (auto) / 3: TMA pipeline

@@ -140,17 +140,11 @@ struct StreamCtx {
   __device__ __forceinline__ T ct(int c, int dy, int dz) const {
     const float* p = crow(c, dy) + dz;
     if constexpr (V == 2) {
-#ifndef SDMP_ODD_PAIR
-#define SDMP_ODD_PAIR 1  // measured faster than two 32-bit loads (r02 A/B)
-#endif
-#if SDMP_ODD_PAIR
+      // odd shift: two aligned 64-bit loads (r02 A/B: faster than two 32-bit)
       if (dz & 1) {
         const V2 lo = vload<2>(p - 1), hi = vload<2>(p + 1);
         return v2pack(v2hi(lo), v2lo(hi));
       }
-#else
-      if (dz & 1) return v2pack(p[0], p[1]);  // odd shift: two 32-bit loads
-#endif
     }
     return vload<V>(p);
   }
@@ -194,32 +188,16 @@ __device__ __forceinline__ void push_vals(const Push& P, int x, int y, int z, co
 }
 
 // masked store of V consecutive values at idx (m0: first point, m1: second)
-// Output stores.  SDMP_STREAM_CS = 1 marks them evict-first (st.global.cs):
-// every output array is far larger than L2, so keeping it out of L2 leaves
-// room for the halo tiles neighbouring CTAs re-read.
-#ifndef SDMP_STREAM_CS
-#define SDMP_STREAM_CS 0
-#endif
-__device__ __forceinline__ void st_out(float* p, float v) {
-#if SDMP_STREAM_CS
-  asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v));
-#else
-  *p = v;
-#endif
-}
+// (r03 A/B: evict-first st.global.cs stores gave nothing here)
 __device__ __forceinline__ void vstore(float* p, int64_t idx, float v, bool m0, bool) {
-  if (m0) st_out(p + idx, v);
+  if (m0) p[idx] = v;
 }
 __device__ __forceinline__ void vstore(float* p, int64_t idx, V2 v, bool m0, bool m1) {
   if (m0 && m1) {
-#if SDMP_STREAM_CS
-    asm volatile("st.global.cs.b64 [%0], %1;" ::"l"(p + idx), "l"(v.r));
-#else
     *reinterpret_cast<uint64_t*>(p + idx) = v.r;
-#endif
   } else {
-    if (m0) st_out(p + idx, v2lo(v));
-    if (m1) st_out(p + idx + 1, v2hi(v));
+    if (m0) p[idx] = v2lo(v);
+    if (m1) p[idx + 1] = v2hi(v);
   }
 }
 
@@ -329,17 +307,13 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
 // x-chunk count: whole waves of one CTA per SM, small priming overhead.
 inline int stream_chunks(int64_t tiles, int nx, int R, int ctas = 1) {
   const int64_t slots = (int64_t)num_sms() * ctas;
-  static const double cta_planes = [] {  // A/B: per-CTA fixed cost in planes
-    const char* e = getenv("SDMP_STREAM_CTA_PLANES");
-    return e ? atof(e) : 0.0;
-  }();
   double best = 1e30;
   int best_n = 1;
   for (int n = 1; n <= 64 && n <= nx; ++n) {
     const int chunk = (nx + n - 1) / n;
     const int64_t items = tiles * ((nx + chunk - 1) / chunk);
     const int64_t waves = (items + slots - 1) / slots;
-    const double cost = (double)waves * (chunk + 0.5 * 2 * R + cta_planes);
+    const double cost = (double)waves * (chunk + 0.5 * 2 * R);
     if (cost < best - 1e-9) {
       best = cost;
       best_n = n;

@@ -94,6 +94,7 @@ def acoustic_case(shape, steps, mode, dims, tag, nrec, src_xyz, rec_yz, f0, h=10
            "wavefield_max_abs": float(np.abs(got - want).max()),
            "wavefield_max": float(np.abs(want).max()),
            "traces_rel_l2": rel_l2(traces, tw), "traces_max_abs": float(np.abs(traces - tw).max()),
+           "traces_max": float(np.abs(tw).max()),
            "tolerance_rel_l2": REL, "gpu_apply_s_incl_plan_build": gpu_s,
            "oracle_s": cpu_s, "oracle_threads": THREADS}
     return res
@@ -114,9 +115,12 @@ def test_c2_downscaled_2x2_full():
     per rank on the (2,2,1) topology in full mode."""
     shape = (256, 256, 128)
     ext = tuple(10.0 * (n - 1) for n in shape)
+    # receiver line through the source depth, crossing the x split (the
+    # wave reaches it within the 30 steps)
     res = acoustic_case(shape, 30, "full", (2, 2, 1), "c2", 64,
                         (0.5 * ext[0] + 3.7, 0.5 * ext[1] + 3.7, 0.5 * ext[2] + 3.7),
-                        (0.5 * ext[1] + 2.5, 20.3), 0.030)
+                        (0.5 * ext[1] + 2.5, 0.5 * ext[2] - 31.3), 0.030)
+    assert res["traces_max"] > 1e-3 * res["wavefield_max"], res
     report("C2_acoustic_so8_128cubed_per_rank_2x2x1_full", res)
     assert res["wavefield_rel_l2"] <= REL and res["traces_rel_l2"] <= REL, res
 
@@ -143,6 +147,9 @@ def test_c3_downscaled_tti_2x1_full():
         sim.write_global(name, kd.fields[name].data_gather().astype(np.float64))
     sim.write_global("p", init.astype(np.float64))
     sim.write_global("r", 0.5 * init.astype(np.float64))
+    # the direction cosines are read at offsets: their halos are exchanged
+    # once before the time loop (the hoisted HaloSpot)
+    sim.exchange_static(("ax", "ay", "az"), (so,) * 3)
     sim.run(0, steps - 1)
     res = {"shape": list(shape), "steps": steps, "mode": mode, "oracle_ranks": list(dims)}
     for name, fn in (("p", p), ("r", r)):

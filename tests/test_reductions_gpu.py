@@ -94,13 +94,15 @@ def test_visco_without_relaxation_reduces_to_elastic(so):
 
 
 def _nested(u0, axis, w1, R):
-    """D_a(D_a u) on the DOMAIN of an array with zero exterior halo >= 2R
-    (the reference's Deriv(a * Deriv) lowering evaluated for a = e_axis)."""
+    """D_a(a_a D_a u) with a_a = 1 on the DOMAIN and 0 in the exterior halo
+    (every field's exterior halo is zero): the reference's
+    Deriv(a * Deriv) lowering for a = e_axis, on an array padded by 2R."""
     pad = np.pad(u0, 2 * R)
     n = u0.shape
     gbox = (tuple(R for _ in n), tuple(3 * R + k for k in n))
+    mask = np.pad(np.ones(n), R)          # a_a on gbox: 1 inside, 0 outside
     g = np.zeros(pad.shape)
-    g[tuple(slice(l, h) for l, h in zip(*gbox))] = K.first_derivative(pad, gbox, axis, w1)
+    g[tuple(slice(l, h) for l, h in zip(*gbox))] = mask * K.first_derivative(pad, gbox, axis, w1)
     box = (tuple(2 * R for _ in n), tuple(2 * R + k for k in n))
     return K.first_derivative(g, box, axis, w1)
 
