@@ -34,6 +34,12 @@ from . import symbolics as S
 from .symbolics import Eq, StencilEquation, solve_forward  # re-exported
 
 _FUNCS: "weakref.WeakValueDictionary" = weakref.WeakValueDictionary()
+GUARD_WORD = 0x7FC0DEAD  # NaN canary of SDMP_GUARD allocations
+
+
+def torch_module():
+    import torch
+    return torch
 
 
 def _torch():
@@ -267,14 +273,37 @@ class Function:
         # the arrays are allocated on the CPU, but apply() refuses to run.
         dev = (torch.device("cuda", grid.ctx.device or 0) if torch.cuda.is_available()
                else torch.device("cpu"))
-        self.storage = torch.zeros((self.time_buffers,) + self.full3, dtype=torch.float32,
-                                   device=dev)
+        shape = (self.time_buffers,) + self.full3
+        self._guard = None
+        if os.environ.get("SDMP_GUARD", "0") != "0":
+            # debug: the buffers sit between two guard zones of at least one
+            # x-plane filled with a NaN canary; check_guard() verifies no
+            # kernel or copy wrote past either end of the allocation
+            # (memory checking without compute-sanitizer)
+            n = math.prod(shape)
+            g = max(16384, self.full3[1] * self.full3[2])
+            g = (g + 255) // 256 * 256
+            flat = torch.full((g + n + g,), float("nan"), dtype=torch.float32, device=dev)
+            flat.view(torch.int32).fill_(GUARD_WORD)
+            self.storage = flat[g:g + n].view(shape)
+            self.storage.zero_()
+            self._guard = (flat, g, n)
+        else:
+            self.storage = torch.zeros(shape, dtype=torch.float32, device=dev)
         self._latest = 0
         # bumped by every Data write: plans re-bind derived buffers (dt^2/m)
         # and re-exchange static halos only when a static field changed
         self._version = 0
 
     # -- storage helpers ---------------------------------------------------
+    def check_guard(self) -> bool:
+        """SDMP_GUARD=1 allocations: both guard zones still hold the canary."""
+        if self._guard is None:
+            return True
+        flat, g, n = self._guard
+        w = flat.view(torch_module().int32)
+        return bool((w[:g] == GUARD_WORD).all()) and bool((w[g + n:] == GUARD_WORD).all())
+
     @property
     def time_buffers(self) -> int:
         return self.spec.time_buffers

@@ -146,7 +146,7 @@ class NativeOperatorPlan:
                 variant = 0
                 if k.m is not None:
                     mfn = op.fields[k.m]
-                    sbuf = torch.empty_like(mfn.storage[0])
+                    sbuf = torch.zeros_like(mfn.storage[0])
                     self.scale_bufs.append((sbuf, mfn, C))
                     if (k.A, k.B, k.p, k.q) == (2, -1, 2, -1):
                         self.cfl.append((k, mfn))

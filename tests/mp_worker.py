@@ -14,6 +14,7 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
@@ -152,6 +153,7 @@ def main():
     steps = int(os.environ.get("STEPS", "12"))
     failures = []
     order_problems = []
+    memory_problems = []
     results = {}
     cases = [("acoustic", acoustic, {}), ("diffusion", diffusion, {}), ("damped", damped, {}),
              ("rotated", rotated, {}), ("tti", tti, {}),
@@ -171,6 +173,10 @@ def main():
             op.apply(time_M=steps - 1, dt=dt, mpi=mode)
             got = [f.data_gather() for f in fields]
             got_tr = rec.data.copy() if rec is not None else None
+            if os.environ.get("SDMP_GUARD", "0") != "0":
+                from memcheck_util import check_fields
+                memory_problems.extend(f"{tag} rank {rank}: {n}: {p}" for n, p in
+                                       check_fields(list(op.fields.values()), g.decomposition, rank))
             if mode == "full" and size > 1:
                 order_problems.extend(f"{fam}: {p}" for p in full_order(op, dt, steps))
             # release the distributed fields before building the reference
@@ -193,12 +199,14 @@ def main():
             A._FUNCS.clear()
             torch.cuda.empty_cache()
     orders = ctx.allgather(order_problems)
+    mem = [p for ps in ctx.allgather(memory_problems) for p in ps]
     if rank == 0:
         print(json.dumps({"topology": topo, "shape": shape, "results": results,
                           "order_ok": not any(orders), "order": orders,
+                          "memory_ok": not mem, "memory": mem[:20],
                           "devices": torch.cuda.device_count(), "ranks": size}))
     ctx.barrier()
-    return 1 if failures or any(orders) else 0
+    return 1 if failures or any(orders) or mem else 0
 
 
 if __name__ == "__main__":

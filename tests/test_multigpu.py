@@ -28,7 +28,9 @@ ALL = "acoustic,diffusion,damped,rotated,tti,elastic,elastic_col,visco"
 
 
 def _env(nproc, **extra):
-    env = dict(os.environ, **extra)
+    # SDMP_GUARD: canary zones around every field + exterior-halo invariant
+    # checked per rank after each run (tests/memcheck_util.py)
+    env = dict(os.environ, SDMP_GUARD="1", **extra)
     ndev = torch.cuda.device_count()
     if nproc > ndev:
         # time-sliced ranks wait longer for each other: a generous watchdog
@@ -60,6 +62,8 @@ def _check(rc, rep, err, families):
     assert not bad, bad
     # full mode kept the Listing-8 order on every rank (post -> CORE -> wait -> OWNED)
     assert rep.get("order_ok", True), rep.get("order")
+    # no write past a field allocation or into an exterior halo on any rank
+    assert rep.get("memory_ok") is True, rep.get("memory")
 
 
 needs_gpu = pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
