@@ -130,6 +130,42 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+class NvlinkCounters:
+    """NVLink data bytes sent / received by this rank's GPU over an interval
+    (NVML field values, cumulative per link, summed over links): the
+    driver-side measurement of the halo traffic, independent of the
+    library's own byte count.  None when NVML does not expose them."""
+
+    def __init__(self, device):
+        self.ok = False
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(device)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def read(self):
+        if not self.ok:
+            return None
+        N = self.N
+        out = {}
+        for name, fid in (("tx", N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX),
+                          ("rx", N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX)):
+            total = 0
+            try:
+                vals = N.nvmlDeviceGetFieldValues(self.h, [(fid, link) for link in range(18)])
+                for v in vals:
+                    if v.nvmlReturn == 0:
+                        total += int(v.value.ullVal)
+            except Exception:
+                return None
+            out[name] = total * 1024  # the THROUGHPUT_DATA fields count KiB
+        return out
+
+
 # ---------------------------------------------------------------------------
 # CPU reference arm / baseline: the oracle port (numpy, fp64) on a slab
 
@@ -350,13 +386,16 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(ctx.device or 0)
     clocks.start()  # before the barrier: its wait for a first sample differs per rank
+    nvl = NvlinkCounters(ctx.device or 0) if N > 1 else None
     ctx.barrier()
     torch.cuda.synchronize()
+    nv0 = nvl.read() if nvl else None
     e0.record(stream)
     nplan.run(t_a, t_a + args.steps - 1, stream)
     e1.record(stream)
     nplan.sync()
     torch.cuda.synchronize()
+    nv1 = nvl.read() if nvl else None
     clk = clocks.stop()
     ctx.barrier()
     ms = e0.elapsed_time(e1)
@@ -468,13 +507,28 @@ def main():
                    "transport": ("fused: OWNED-slab kernels store into peer halos (NVLink)"
                                  if fused else "copy engines (cudaMemcpy3DAsync, 4 streams)"),
                    "post_ms_rank0": post_ms,
-                   "link_gbs_rank0": (sent / (post_ms * 1e-3) / 1e9
-                                      if post_ms > 0 and not fused else None),
+                   # fused: bytes pushed / time of the slab kernels that push them
+                   # (a lower bound on the link rate: the stores are spread
+                   # over the slabs' compute)
+                   "link_gbs_rank0": (sent / (post_ms * 1e-3) / 1e9 if post_ms > 0 else None),
                    "link_peak_gbs": 900.0}
         if fused:
             exposed["link_note"] = ("halos are stored by the OWNED-slab kernels while they "
                                     "compute (no separate transfer to time); post_ms_rank0 is "
                                     "the slab kernels' time, the exposed time is the cost")
+        if nv0 and nv1:
+            # NVML NVLink data counters over the timed region (rank 0's GPU)
+            tx = (nv1["tx"] - nv0["tx"]) / args.steps
+            rx = (nv1["rx"] - nv0["rx"]) / args.steps
+            exposed["nvlink_counters_rank0"] = {
+                "tx_bytes_per_step": tx, "rx_bytes_per_step": rx,
+                "tx_gbs_step_avg": tx / (ms_max / args.steps * 1e-3) / 1e9,
+                "tx_gbs_during_transfer": (tx / (post_ms * 1e-3) / 1e9) if post_ms > 0 else None,
+                "transfer_window": ("OWNED-slab kernels (fused push)" if fused
+                                    else "copy-engine posts"),
+                "peak_gbs_per_direction": 900.0,
+                "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX, summed over links"}
+
 
     # per-rank action timings (skew between ranks shows up as WAIT time)
     rank_actions = ctx.allgather([[int(r[2]), round(r[4], 4)] for r in rows]) if N > 1 else None

@@ -265,6 +265,14 @@ class NativeOperatorPlan:
         # (default: copy engines, cudaMemcpy3DAsync)
         eng = 1 if os.environ.get("SDMP_COPY_ENGINE", "ce") == "sm" else 0
         ints = [R.ACT["POST"], a.stream, a.phase, 0, (16 if a.pushed else 0) | eng]
+        # z is never split: its halo (and padding) is exterior on every rank,
+        # zero on sender and receiver alike, so each message ships whole
+        # FULL-z rows -- an x-face becomes R contiguous (ny x full_z) blocks
+        # and a y-face nx contiguous (R x full_z) blocks instead of R*ny or
+        # nx*R separate nz-float rows (fewer, larger copy-engine bursts);
+        # the receiver's z halo is rewritten with the zeros it holds
+        whole_z = (decomp.ndims == 3 and decomp.topology.dims[2] == 1
+                   and os.environ.get("SDMP_WHOLE_Z", "1") != "0")
         n = 0
         for m in a.messages:
             for f, t in a.spot.fields:
@@ -272,6 +280,8 @@ class NativeOperatorPlan:
                 slo = [l + h for l, h in zip(m.send[0], fn.halo3)] + [0] * (3 - len(m.send[0]))
                 ext = [u - l for l, u in zip(*m.send)] + [1] * (3 - len(m.send[0]))
                 dlo = [l + h for l, h in zip(m.recv[0], fn.halo3)] + [0] * (3 - len(m.recv[0]))
+                if whole_z and ext[2] == fn.local3[2]:
+                    slo[2], dlo[2], ext[2] = 0, 0, fn.full3[2]
                 ints += [fid[f], t, pfid[(m.peer, f)]] + slo + dlo + ext
                 n += 1
         ints[3] = n

@@ -135,3 +135,55 @@ def test_rotated_axis_aligned_reduces_to_nested_second_derivative(so, direction,
         u2, u0 = u0, u1
     e = rel_l2(got, u0)
     assert e <= REL, (e, np.abs(got - u0).max())
+
+
+@pytest.mark.parametrize("so", [4, 8])
+@pytest.mark.parametrize("mode", ["diagonal", "full"])
+def test_staggered_elastic_fluid_limit_is_second_order_acoustic(so, mode):
+    """Staggered elastic with mu = 0, equal normal
+    stresses s and zero shear / velocity initially: the shear stresses stay
+    0, the three normal stresses stay equal, and eliminating v gives the
+    single-field recurrence s1 = 2 s0 - s2 + dt^2 lam sum_a D-_a(b D+_a s0)
+    (s2 = s0 on the first step), with v = b D+ s zero outside the DOMAIN
+    (exterior halo).  Checked against that recurrence evaluated in fp64 with
+    the staggered weights of the reference's solver."""
+    shape, steps = (32, 28, 36), 10
+    grid = Grid(shape, tuple(10.0 * (n - 1) for n in shape))
+    el = KD.elastic_model(grid, so=so)
+    el.fields["mu"].data[...] = 0.0
+    rng = np.random.default_rng(21)
+    s0 = np.float32(rng.standard_normal(shape))
+    for n in ("txx", "tyy", "tzz"):
+        el.fields[n].data[...] = s0
+    dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.1)))
+    Operator([el]).apply(time_M=steps - 1, dt=dt, mpi=mode)
+    got = {n: el.fields[n].data_gather() for n in KD.VNAMES + KD.TNAMES}
+    for n in ("txy", "txz", "tyz"):
+        assert not np.any(got[n]), n
+    assert np.array_equal(got["txx"], got["tyy"]) and np.array_equal(got["txx"], got["tzz"])
+
+    R = so // 2
+    sc = [np.float32([float(c) / h for c in S.staggered_coefficients(so)]).astype(np.float64)
+          for h in grid.spacing]
+    b = el.fields["b"].data_gather().astype(np.float64)
+    lam = el.fields["lam"].data_gather().astype(np.float64)
+    dtf = float(np.float32(dt))
+    pad = 2 * R
+
+    def lap_stag(s):
+        sp = np.pad(s, pad)
+        dom = (tuple(pad for _ in shape), tuple(pad + n for n in shape))
+        out = np.zeros(shape)
+        for a in range(3):
+            w = np.zeros(sp.shape)
+            w[tuple(slice(l, h) for l, h in zip(*dom))] = b * K.dplus(sp, dom, a, sc[a])
+            out += K.dminus(w, dom, a, sc[a])
+        return out
+
+    prev = cur = s0.astype(np.float64)
+    for _ in range(steps):
+        nxt = 2.0 * cur - prev + dtf * dtf * lam * lap_stag(cur)
+        prev, cur = cur, nxt
+    e = rel_l2(got["txx"], cur)
+    assert np.abs(cur).max() > 0
+    assert e <= REL, (e, np.abs(got["txx"] - cur).max())
