@@ -259,6 +259,9 @@ template <bool COL = false>
 struct VelOpT {
   static constexpr int NF = 3, NC = 5, NP = 4;
   static constexpr int kCtas = SDMP_VEL_CTAS;
+  // centre tiles tapped along one axis stage only that halo: tyy, txy (y),
+  // tzz, txz (z); tyz both (r04: -18% / -35% staged bytes at SO-8 / SO-16)
+  static constexpr unsigned kCHalo = 1u | (2u << 2) | (1u << 4) | (2u << 6) | (3u << 8);
   float* out[3];
   ElCoef k;
   template <int R, class Ctx>

@@ -7,7 +7,9 @@
 // Per pipeline iteration i (plane xa-R+i):
 //
 //   NF "front" tiles  [TY][32V]              -> per-field x-window registers
-//   NC "centre" tiles [TY+2R][32V+2*OFF]     -> y / z taps (TMA zero-fills OOB)
+//   NC "centre" tiles [TY+2R][32V+2*OFF]     -> y / z taps (TMA zero-fills OOB;
+//                                               an op can drop the y or z halo
+//                                               of a tile tapped along one axis)
 //   NP "point" tiles  [TY][32V]              -> pointwise operands
 //
 // front tiles run 2R planes ahead of the centre/point tiles, so at
@@ -37,21 +39,41 @@ constexpr int kSZ = 32;  // lanes along z
 
 __host__ __device__ constexpr int sround4(int r) { return (r + 3) & ~3; }
 
-template <int R, int TY, int V, int NF, int NC, int NP, int CT = 1>
+// Centre-tile halo mask: 2 bits per centre tile c (bit 2c: the tile carries
+// the R-row y halo, bit 2c+1: the OFF-column z halo).  An op whose tile is
+// only tapped along one axis stages just that halo (Op::kCHalo; default all
+// tiles carry both).
+constexpr unsigned kHaloYZ = 0xFFFFFFFFu;
+__host__ __device__ constexpr bool halo_y(unsigned m, int c) { return (m >> (2 * c)) & 1u; }
+__host__ __device__ constexpr bool halo_z(unsigned m, int c) { return (m >> (2 * c + 1)) & 1u; }
+
+template <int R, int TY, int V, int NF, int NC, int NP, int CT = 1, unsigned M = kHaloYZ>
 struct SLayout {
   static constexpr int TZ = kSZ * V;
   static constexpr int OFF = sround4(R);
-  static constexpr int CZ = TZ + 2 * OFF;
-  static constexpr int CY = TY + 2 * R;
   static constexpr int FRONT = TZ * TY * 4;
-  static constexpr int CENTER = ((CZ * CY * 4) + 127) & ~127;
-  static constexpr int STAGE = NF * FRONT + NC * CENTER + NP * FRONT;
+  // centre tile c: rows (y halo R each side if masked in), columns (z halo OFF)
+  static constexpr int cy(int c) { return TY + (halo_y(M, c) ? 2 * R : 0); }
+  static constexpr int cz(int c) { return TZ + (halo_z(M, c) ? 2 * OFF : 0); }
+  static constexpr int cbytes(int c) { return ((cz(c) * cy(c) * 4) + 127) & ~127; }
+  static constexpr int coff(int c) {
+    int o = 0;
+    for (int i = 0; i < c; ++i) o += cbytes(i);
+    return o;
+  }
+  static constexpr int ctx_bytes() {
+    int b = 0;
+    for (int i = 0; i < NC; ++i) b += cz(i) * cy(i) * 4;
+    return b;
+  }
+  static constexpr int CENTERS = coff(NC);
+  static constexpr int STAGE = NF * FRONT + CENTERS + NP * FRONT;
   static constexpr int S0 = (220 * 1024) / CT / STAGE;  // CT resident CTAs per SM
   static constexpr int S = S0 > 4 ? 4 : (S0 < 2 ? 2 : S0);
   static constexpr int BYTES = S * STAGE + 2 * S * 8;
   static constexpr int THREADS = 32 * (TY + 1);
   static constexpr uint32_t TX_FRONT = NF * FRONT;
-  static constexpr uint32_t TX_MAIN = NF * FRONT + NC * CZ * CY * 4 + NP * FRONT;
+  static constexpr uint32_t TX_MAIN = NF * FRONT + ctx_bytes() + NP * FRONT;
 };
 
 constexpr int kMaxMaps = 24;
@@ -102,6 +124,15 @@ constexpr int unroll_for() {
   return SDMP_STREAM_UNROLL ? SDMP_STREAM_UNROLL : (R >= UnrollMinR<Op>::value ? 2 : 1);
 }
 
+template <class Op, class = void>
+struct CHaloOf {
+  static constexpr unsigned value = kHaloYZ;
+};
+template <class Op>
+struct CHaloOf<Op, std::void_t<decltype(Op::kCHalo)>> {
+  static constexpr unsigned value = Op::kCHalo;
+};
+
 template <int V> struct VType;
 template <> struct VType<1> { using T = float; };
 template <> struct VType<2> { using T = V2; };
@@ -118,9 +149,9 @@ __device__ __forceinline__ V2 vload<2>(const float* p) {
 }
 
 // Consumer-side view of one thread's V points.
-template <int R, int TY, int V, int NF, int NC, int NP, int U = 1>
+template <int R, int TY, int V, int NF, int NC, int NP, int U = 1, unsigned M = kHaloYZ>
 struct StreamCtx {
-  using L = SLayout<R, TY, V, NF, NC, NP>;
+  using L = SLayout<R, TY, V, NF, NC, NP, 1, M>;
   using T = typename VType<V>::T;
   static constexpr int W = 2 * R + 1;
   static constexpr int WB = W + U - 1;
@@ -133,8 +164,9 @@ struct StreamCtx {
   // plane x + k of front field f
   __device__ __forceinline__ T xt(int f, int k) const { return w[f][base + R + k]; }
   __device__ __forceinline__ const float* crow(int c, int dy) const {
-    const float* base = reinterpret_cast<const float*>(stage + NF * L::FRONT + c * L::CENTER);
-    return base + (warp + R + dy) * L::CZ + L::OFF + V * lane;
+    const float* base = reinterpret_cast<const float*>(stage + NF * L::FRONT + L::coff(c));
+    return base + (warp + (halo_y(M, c) ? R : 0) + dy) * L::cz(c) + (halo_z(M, c) ? L::OFF : 0) +
+           V * lane;
   }
   // centre tile c at (y + dy, z + dz)
   __device__ __forceinline__ T ct(int c, int dy, int dz) const {
@@ -154,7 +186,7 @@ struct StreamCtx {
     if (push->ndir) push_vals(*push, x, y, z, v, n, m0, m1);
   }
   __device__ __forceinline__ T pt(int q) const {
-    const float* base = reinterpret_cast<const float*>(stage + NF * L::FRONT + NC * L::CENTER +
+    const float* base = reinterpret_cast<const float*>(stage + NF * L::FRONT + L::CENTERS +
                                                        q * L::FRONT);
     return vload<V>(base + warp * L::TZ + V * lane);
   }
@@ -207,7 +239,8 @@ __global__ void __launch_bounds__(SLayout<R, TY, V, Op::NF, Op::NC, Op::NP>::THR
 stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, const int xchunk,
               const __grid_constant__ Push push) {
   constexpr int NF = Op::NF, NC = Op::NC, NP = Op::NP;
-  using L = SLayout<R, TY, V, NF, NC, NP, ctas_for<Op, TY>()>;
+  constexpr unsigned M = CHaloOf<Op>::value;
+  using L = SLayout<R, TY, V, NF, NC, NP, ctas_for<Op, TY>(), M>;
   using T = typename VType<V>::T;
   // __align__(1024) keeps TMA destinations aligned without integer pointer
   // arithmetic, so the consumers keep shared-space pointers (LDS)
@@ -248,11 +281,11 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
           const int x = xa + i - 2 * R;
 #pragma unroll
           for (int c = 0; c < NC; ++c)
-            tma_load_3d(st + NF * L::FRONT + c * L::CENTER, &maps.m[NF + c], &full_bar[s],
-                        z0 - L::OFF, y0 - R, x);
+            tma_load_3d(st + NF * L::FRONT + L::coff(c), &maps.m[NF + c], &full_bar[s],
+                        z0 - (halo_z(M, c) ? L::OFF : 0), y0 - (halo_y(M, c) ? R : 0), x);
 #pragma unroll
           for (int q = 0; q < NP; ++q)
-            tma_load_3d(st + NF * L::FRONT + NC * L::CENTER + q * L::FRONT,
+            tma_load_3d(st + NF * L::FRONT + L::CENTERS + q * L::FRONT,
                         &maps.m[NF + NC + q], &full_bar[s], z0, y0, x);
         }
       }
@@ -290,7 +323,7 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
                                      warp * L::TZ + V * lane);
         if (i >= 2 * R && active) {
           const int x = xa + i - 2 * R;
-          StreamCtx<R, TY, V, NF, NC, NP, U> ctx{w, st, warp, lane, u, &push, x, y, z};
+          StreamCtx<R, TY, V, NF, NC, NP, U, M> ctx{w, st, warp, lane, u, &push, x, y, z};
           op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0, m1);
         }
         __syncwarp();
@@ -327,7 +360,7 @@ inline int stream_chunks(int64_t tiles, int nx, int R, int ctas = 1) {
 template <int R, int TY, int V, class Op>
 int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const float* const* ptrs,
                      cudaStream_t st, const Push* push = nullptr) {
-  using L = SLayout<R, TY, V, Op::NF, Op::NC, Op::NP, ctas_for<Op, TY>()>;
+  using L = SLayout<R, TY, V, Op::NF, Op::NC, Op::NP, ctas_for<Op, TY>(), CHaloOf<Op>::value>;
   static_assert(Op::NF + Op::NC + Op::NP <= kMaxMaps, "too many tensor maps");
   static int attr_dev = -1;
   int dev = 0;
@@ -344,7 +377,7 @@ int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const f
     if (rc) return rc;
   }
   for (int c = 0; c < Op::NC; ++c, ++k) {
-    int rc = make_tmap_3d(&maps.m[k], ptrs[k], full, L::CZ, L::CY, false);
+    int rc = make_tmap_3d(&maps.m[k], ptrs[k], full, L::cz(c), L::cy(c), false);
     if (rc) return rc;
   }
   for (int q = 0; q < Op::NP; ++q, ++k) {

@@ -275,6 +275,8 @@ struct UAcc {
 struct UOp {
   static constexpr int NF = 4, NC = 5, NP = 6;
   static constexpr int kCtas = SDMP_UOP_CTAS;
+  // a_y is tapped along y only, a_z along z only: they stage one halo
+  static constexpr unsigned kCHalo = 1u | (2u << 2) | (3u << 4) | (3u << 6) | (3u << 8);
   float* out[2];
   TTICoef k;
   template <int R, class Ctx>
@@ -331,6 +333,7 @@ struct RUAcc {
 
 struct RUOp {
   static constexpr int NF = 2, NC = 3, NP = 3;
+  static constexpr unsigned kCHalo = 1u | (2u << 2) | (3u << 4);  // a_y: y, a_z: z, g: both
   float* out;
   TTICoef k;
   template <int R, class Ctx>
@@ -379,9 +382,14 @@ static int launch_tti_stream(const Op& op, const Geom& g, const int64_t full[3],
 #ifndef SDMP_TTI_UVW
 #define SDMP_TTI_UVW 2
 #endif
-    constexpr int TYW = upd ? SDMP_TTI_UTYW : (R <= 6 ? 16 : SDMP_TTI_GTYW);
+    // 9-warp CTAs (8 rows + producer) are register-capped at 168 per thread
+    // (ptxas rounds the CTA up to 12 warps): the update pass at R >= 7
+    // needs more, so it runs 7-row tiles (8 warps, 255 registers, no spills)
+    constexpr int TYU = R >= 7 ? 7 : SDMP_TTI_UTYW;
+    constexpr int TYW = upd ? TYU : (R <= 6 ? 16 : SDMP_TTI_GTYW);
     constexpr int VW = upd ? SDMP_TTI_UVW : 2;
-    if (ny <= 8) return launch_stream_op<R, 8, VW>(op, g, full, arrs, st, push);
+    constexpr int TYT = upd && R >= 7 ? 7 : 8;
+    if (ny <= 8) return launch_stream_op<R, TYT, VW>(op, g, full, arrs, st, push);
     return launch_stream_op<R, TYW, VW>(op, g, full, arrs, st, push);
   }
 }

@@ -172,8 +172,9 @@ def test_star_kernels_bitwise_equal_generic(so, monkeypatch):
     assert np.abs(outs[0][0]).max() > 0
 
 
-@pytest.mark.parametrize("family,so", [("tti", 8), ("tti", 12), ("elastic", 8), ("elastic", 4),
-                                       ("visco", 16), ("visco", 8)])
+@pytest.mark.parametrize("family,so", [("tti", 8), ("tti", 12), ("tti", 16), ("elastic", 8),
+                                       ("elastic", 4), ("elastic", 16), ("visco", 16),
+                                       ("visco", 8)])
 def test_stream_kernels_bitwise_equal_generic(family, so, monkeypatch):
     """TMA streaming launches (thick boxes) and generic launches (thin OWNED
     slabs) share one per-point routine: results must agree bit for bit."""
