@@ -154,15 +154,18 @@ class NvlinkCounters:
         out = {}
         for name, fid in (("tx", N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX),
                           ("rx", N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX)):
-            total = 0
+            total, ok = 0, 0
             try:
+                # scopeId = link id; links that do not exist return an error
                 vals = N.nvmlDeviceGetFieldValues(self.h, [(fid, link) for link in range(18)])
                 for v in vals:
                     if v.nvmlReturn == 0:
                         total += int(v.value.ullVal)
+                        ok += 1
             except Exception:
                 return None
             out[name] = total * 1024  # the THROUGHPUT_DATA fields count KiB
+            out[name + "_links"] = ok
         return out
 
 
@@ -386,18 +389,20 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(ctx.device or 0)
     clocks.start()  # before the barrier: its wait for a first sample differs per rank
+    # NVLink counters are read OUTSIDE the barrier-bracketed region: an NVML
+    # query takes milliseconds and would skew the ranks' start times
     nvl = NvlinkCounters(ctx.device or 0) if N > 1 else None
+    nv0 = nvl.read() if nvl else None
     ctx.barrier()
     torch.cuda.synchronize()
-    nv0 = nvl.read() if nvl else None
     e0.record(stream)
     nplan.run(t_a, t_a + args.steps - 1, stream)
     e1.record(stream)
     nplan.sync()
     torch.cuda.synchronize()
-    nv1 = nvl.read() if nvl else None
     clk = clocks.stop()
     ctx.barrier()
+    nv1 = nvl.read() if nvl else None
     ms = e0.elapsed_time(e1)
     ms_max = ctx.allreduce_max(ms)
     # two more repetitions of the same K steps (reported, not the value):
