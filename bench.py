@@ -164,6 +164,8 @@ class NvlinkCounters:
                         ok += 1
             except Exception:
                 return None
+            if ok == 0:
+                return None  # NOT_SUPPORTED (e.g. counters hidden on this box)
             out[name] = total * 1024  # the THROUGHPUT_DATA fields count KiB
             out[name + "_links"] = ok
         return out
@@ -521,6 +523,9 @@ def main():
             exposed["link_note"] = ("halos are stored by the OWNED-slab kernels while they "
                                     "compute (no separate transfer to time); post_ms_rank0 is "
                                     "the slab kernels' time, the exposed time is the cost")
+        if not (nv0 and nv1):
+            exposed["nvlink_counters_rank0"] = ("unavailable: NVML reports the NVLink data "
+                                                "counters as not supported on this box")
         if nv0 and nv1:
             # NVML NVLink data counters over the timed region (rank 0's GPU)
             tx = (nv1["tx"] - nv0["tx"]) / args.steps

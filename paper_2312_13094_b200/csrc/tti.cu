@@ -423,9 +423,25 @@ static int variant_env() {
   return e ? atoi(e) : 0;
 }
 
+#include "tti_fused.cuh"
+
 template <int R>
 static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const Push& push) {
-  // pass 1 on the box grown by R (g is read up to R away by pass 2)
+  if constexpr (R <= 4) {
+    // SO <= 8: single pass (tti_fused.cuh); its generic twin for boxes the
+    // TMA loads cannot cover and for the bitwise tests (SDMP_TTI_VARIANT=1)
+    const float* in[10] = {p.tap[TP], p.pnt[QP2], p.tap[TR], p.pnt[QR2], p.pnt[QM],
+                           p.pnt[QE], p.pnt[QD], p.pnt[QAX], p.pnt[QAY], p.pnt[QAZ]};
+    if (variant_env() != 1 && fused_fits<R>(p.g) && tma_ok(full, in, 10))
+      return launch_fused<R>(p, st, full, push);
+    dim3 b(32, 8);
+    dim3 g2((p.g.hi[2] - p.g.lo[2] + 31) / 32, (p.g.hi[1] - p.g.lo[1] + 7) / 8,
+            p.g.hi[0] - p.g.lo[0]);
+    tti_fused_generic<R><<<g2, b, 0, st>>>(p, push);
+    SDMP_LAUNCHED();
+    return SDMP_OK;
+  }
+  // SO > 8: two passes.  Pass 1 on the box grown by R (g is read up to R away by pass 2)
   TTIGeneric p1 = p;
   for (int a = 0; a < 3; ++a) {
     p1.g.lo[a] = p.g.lo[a] - R;
