@@ -427,9 +427,15 @@ static int variant_env() {
 
 template <int R>
 static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const Push& push) {
-  if constexpr (R <= 4) {
-    // SO <= 8: single pass (tti_fused.cuh); its generic twin for boxes the
-    // TMA loads cannot cover and for the bitwise tests (SDMP_TTI_VARIANT=1)
+#ifndef SDMP_TTI_FUSED_MAXR
+#define SDMP_TTI_FUSED_MAXR 2
+#endif
+  if constexpr (R <= SDMP_TTI_FUSED_MAXR) {
+    // single pass (tti_fused.cuh) where it beats the two passes (r04, 512^3:
+    // SO-4 87.0 vs 70.1 GPts/s; SO-8 51.9 vs 65.8 -- at R = 4 the 2R halo
+    // rows double the g work of an 8-row tile); its
+    // generic twin for boxes the TMA loads cannot cover and for the bitwise
+    // tests (SDMP_TTI_VARIANT=1)
     const float* in[10] = {p.tap[TP], p.pnt[QP2], p.tap[TR], p.pnt[QR2], p.pnt[QM],
                            p.pnt[QE], p.pnt[QD], p.pnt[QAX], p.pnt[QAY], p.pnt[QAZ]};
     if (variant_env() != 1 && fused_fits<R>(p.g) && tma_ok(full, in, 10))
