@@ -361,7 +361,10 @@ static int launch_el_stream(const Op& op, const Geom& g, const int64_t full[3],
   constexpr bool vel = Op::NP <= 4, visco = Op::NP == 15;
   constexpr int V = (visco && R > 4) ? 1 : ((vel && R > 4) ? SDMP_VEL_VW : 2);
   constexpr int TYN = vel ? SDMP_VEL_TYN : (visco ? 16 : 8);
-  constexpr int TYW = vel ? SDMP_VEL_TYW : 8;
+#ifndef SDMP_STRESS_TYW
+#define SDMP_STRESS_TYW 8
+#endif
+  constexpr int TYW = vel ? SDMP_VEL_TYW : SDMP_STRESS_TYW;
   const int ny = g.hi[1] - g.lo[1];
   if constexpr (R <= 4) {
     if (ny <= 4) return launch_stream_op<R, 4, V>(op, g, full, arrs, st, &push);

@@ -385,10 +385,13 @@ static int launch_tti_stream(const Op& op, const Geom& g, const int64_t full[3],
     // 9-warp CTAs (8 rows + producer) are register-capped at 168 per thread
     // (ptxas rounds the CTA up to 12 warps): the update pass at R >= 7
     // needs more, so it runs 7-row tiles (8 warps, 255 registers, no spills)
-    constexpr int TYU = R >= 7 ? 7 : SDMP_TTI_UTYW;
+#ifndef SDMP_TTI_UTY7_MINR
+#define SDMP_TTI_UTY7_MINR 7
+#endif
+    constexpr int TYU = R >= SDMP_TTI_UTY7_MINR ? 7 : SDMP_TTI_UTYW;
     constexpr int TYW = upd ? TYU : (R <= 6 ? 16 : SDMP_TTI_GTYW);
     constexpr int VW = upd ? SDMP_TTI_UVW : 2;
-    constexpr int TYT = upd && R >= 7 ? 7 : 8;
+    constexpr int TYT = upd && R >= SDMP_TTI_UTY7_MINR ? 7 : 8;
     if (ny <= 8) return launch_stream_op<R, TYT, VW>(op, g, full, arrs, st, push);
     return launch_stream_op<R, TYW, VW>(op, g, full, arrs, st, push);
   }
@@ -439,7 +442,7 @@ static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const P
     const float* in[10] = {p.tap[TP], p.pnt[QP2], p.tap[TR], p.pnt[QR2], p.pnt[QM],
                            p.pnt[QE], p.pnt[QD], p.pnt[QAX], p.pnt[QAY], p.pnt[QAZ]};
     if (variant_env() != 1 && fused_fits<R>(p.g) && tma_ok(full, in, 10))
-      return launch_fused<R>(p, st, full, push);
+      return launch_fused<R, 2>(p, st, full, push);
     dim3 b(32, 8);
     dim3 g2((p.g.hi[2] - p.g.lo[2] + 31) / 32, (p.g.hi[1] - p.g.lo[1] + 7) / 8,
             p.g.hi[0] - p.g.lo[0]);
@@ -542,6 +545,21 @@ int tti_update_entry(cudaStream_t st, const float* const in[10], float* p1, floa
 
 template <int R>
 static int launch_rot(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const Push& push) {
+#ifndef SDMP_ROT_FUSED_MAXR
+#define SDMP_ROT_FUSED_MAXR 2
+#endif
+  if constexpr (R <= SDMP_ROT_FUSED_MAXR) {
+    // single pass for the narrow stencils, as for TTI (tti_fused.cuh, NF = 1)
+    const float* in[6] = {p.tap[TP], p.pnt[QP2], p.pnt[QM], p.pnt[QAX], p.pnt[QAY], p.pnt[QAZ]};
+    if (variant_env() != 1 && fused_fits<R>(p.g) && tma_ok(full, in, 6))
+      return launch_fused<R, 1>(p, st, full, push);
+    dim3 b(32, 8);
+    dim3 g2((p.g.hi[2] - p.g.lo[2] + 31) / 32, (p.g.hi[1] - p.g.lo[1] + 7) / 8,
+            p.g.hi[0] - p.g.lo[0]);
+    rot_fused_generic<R><<<g2, b, 0, st>>>(p, push);
+    SDMP_LAUNCHED();
+    return SDMP_OK;
+  }
   TTIGeneric p1 = p;
   for (int a = 0; a < 3; ++a) {
     p1.g.lo[a] = p.g.lo[a] - R;

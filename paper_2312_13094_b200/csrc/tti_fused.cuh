@@ -32,8 +32,11 @@
 constexpr int kFTY = 8;   // tile rows
 constexpr int kFTZ = 64;  // tile columns (32 lanes x 2)
 
-template <int R>
+// NF = 2: the TTI pair (p, r); NF = 1: the single-field rotated operator
+// (the SPEC's tti_gxx_kernel, u1 = 2 u0 - u2 + dt^2/m G u0)
+template <int R, int NF = 2>
 struct FLayout {
+  static constexpr int NPT = NF == 2 ? 5 : 2;  // p2 r2 m epsp delp | u2 m
   static constexpr int OFF = sround4(R);
   static constexpr int GY = kFTY + 2 * R;   // g-region rows
   static constexpr int GZ = kFTZ + 2 * OFF; // g-region columns
@@ -43,20 +46,22 @@ struct FLayout {
   static constexpr int CEN = ((CY * CZ * 4) + 127) & ~127;
   static constexpr int PTB = kFTY * kFTZ * 4;
   // stage: fronts p, r (g-region, plane x'+R) | centres p, r (plane x') |
-  // a_x, a_y, a_z (g-region, plane x') | p2, r2, m, epsp, delp (tile, plane x'-R)
-  static constexpr int O_FP = 0, O_FR = GREG, O_CP = 2 * GREG, O_CR = 2 * GREG + CEN;
-  static constexpr int O_A = 2 * GREG + 2 * CEN;  // + q * GREG
-  static constexpr int O_PT = 5 * GREG + 2 * CEN; // + q * PTB
-  static constexpr int STAGE = O_PT + 5 * PTB;
+  // a_x, a_y, a_z (g-region, plane x') | pointwise (tile, plane x'-R)
+  static constexpr int O_FP = 0, O_FR = (NF - 1) * GREG, O_CP = NF * GREG;
+  static constexpr int O_CR = NF * GREG + (NF - 1) * CEN;
+  static constexpr int O_A = NF * GREG + NF * CEN;          // + q * GREG
+  static constexpr int O_PT = (NF + 3) * GREG + NF * CEN;   // + q * PTB
+  static constexpr int STAGE = O_PT + NPT * PTB;
   static constexpr int S = 3;
-  static constexpr int PLANE = 4 * GREG;  // a_y g_p, a_y g_r, a_z g_p, a_z g_r
+  // product plane: a_y g (per field), then a_z g (per field)
+  static constexpr int PLANE = 2 * NF * GREG;
   static constexpr int BYTES = S * STAGE + 2 * PLANE + 2 * S * 8;
   static constexpr int NHW = R;                 // halo warps (2 rows each)
   static constexpr int NCW = kFTY + NHW + 1;    // consumer warps
   static constexpr int THREADS = 32 * (NCW + 1);
-  static constexpr uint32_t TX_FRONT = 2 * GY * GZ * 4;
-  static constexpr uint32_t TX_G = 2 * CY * CZ * 4 + 3 * GY * GZ * 4;
-  static constexpr uint32_t TX_PT = 5 * PTB;
+  static constexpr uint32_t TX_FRONT = NF * GY * GZ * 4;
+  static constexpr uint32_t TX_G = NF * CY * CZ * 4 + 3 * GY * GZ * 4;
+  static constexpr uint32_t TX_PT = NPT * PTB;
 };
 
 struct FusedTTI {
@@ -69,7 +74,7 @@ struct FusedTTI {
 template <int R, int W>
 struct FAcc {
   using T = V2;
-  using L = FLayout<R>;
+  using L = FLayout<R>;  // CZ does not depend on NF
   const V2 (&wp)[W];
   const V2 (&wr)[W];
   const float* cp;  // centre p at this pair (centre row / column already applied)
@@ -147,15 +152,16 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // ROLE 0: tile row (g, product planes, x scatter, Laplacian, outer y / z
 // derivative, update); ROLE 1: two halo rows (g, a_y g); ROLE 2: the z-halo
 // columns of the tile rows (g, a_z g)
-template <int R, int ROLE>
+template <int R, int ROLE, int NF>
 __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char* plane,
                                                uint64_t* full_bar, uint64_t* empty_bar,
                                                const FusedTTI& P, const Push& push, int xa,
                                                int nit, int z0, int y0, int warp, int lane) {
-  using L = FLayout<R>;
+  using L = FLayout<R, NF>;
   constexpr int W = 2 * R + 1;
   constexpr int NP = ROLE == 1 ? 2 : 1;  // point pairs of this thread
   constexpr int GQ = L::GREG / 4;
+  constexpr int NA = ROLE == 0 ? W : 1;
   const Geom& g = P.g;
   int gr[NP], gc;
   if (ROLE == 0) {
@@ -180,14 +186,14 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
   const bool m0 = yin && z >= g.lo[2] && z < g.hi[2];
   const bool m1 = yin && z + 1 >= g.lo[2] && z + 1 < g.hi[2];
 
-  V2 wp[NP][W], wr[NP][W];             // x-windows (planes x'-R .. x'+R after the load)
-  V2 accp[ROLE == 0 ? W : 1], accr[ROLE == 0 ? W : 1];  // outputs x'-R .. x'+R
+  V2 wp[NP][W], wr[NP][W];  // x-windows (planes x'-R .. x'+R after the load)
+  V2 accp[NA], accr[NA];    // outputs x'-R .. x'+R (tile role)
 #pragma unroll
   for (int k = 0; k < W; ++k)
 #pragma unroll
     for (int j = 0; j < NP; ++j) wp[j][k] = wr[j][k] = v2bcast(0.f);
 #pragma unroll
-  for (int k = 0; k < (ROLE == 0 ? W : 1); ++k) accp[k] = accr[k] = v2bcast(0.f);
+  for (int k = 0; k < NA; ++k) accp[k] = accr[k] = v2bcast(0.f);
   V2 lapv = v2bcast(0.f);
 
   for (int i = 0; i < nit; ++i) {
@@ -201,11 +207,11 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
 #pragma unroll
       for (int k = 0; k < W - 1; ++k) {
         wp[j][k] = wp[j][k + 1];
-        wr[j][k] = wr[j][k + 1];
+        if (NF == 2) wr[j][k] = wr[j][k + 1];
       }
       const int o = gr[j] * L::GZ + gc;
       wp[j][W - 1] = vload<2>(reinterpret_cast<const float*>(st + L::O_FP) + o);
-      wr[j][W - 1] = vload<2>(reinterpret_cast<const float*>(st + L::O_FR) + o);
+      if (NF == 2) wr[j][W - 1] = vload<2>(reinterpret_cast<const float*>(st + L::O_FR) + o);
     }
     const bool gpl = i >= 2 * R;
     // (b) g at this thread's points, product planes, x scatter, Laplacian
@@ -215,18 +221,22 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
         const int o = gr[j] * L::GZ + gc;
         const int oc = (gr[j] + R) * L::CZ + gc + L::OFF;
         const float* A = reinterpret_cast<const float*>(st + L::O_A);
-        FAcc<R, W> a{wp[j], wr[j], reinterpret_cast<const float*>(st + L::O_CP) + oc,
+        FAcc<R, W> a{wp[j], NF == 2 ? wr[j] : wp[j],
+                     reinterpret_cast<const float*>(st + L::O_CP) + oc,
                      reinterpret_cast<const float*>(st + L::O_CR) + oc, vload<2>(A + o),
                      vload<2>(A + GQ + o), vload<2>(A + 2 * GQ + o)};
-        V2 gp, grv;
-        g_point<R>(a, P.c, gp, grv);
+        V2 gp, grv = v2bcast(0.f);
+        if constexpr (NF == 2)
+          g_point<R>(a, P.c, gp, grv);
+        else
+          gp = g1_point<R>(a, P.c);
         if (ROLE != 2) {  // a_y g: tapped along y (tile and halo rows)
           *reinterpret_cast<uint64_t*>(pl + o) = vmul(a.ay, gp).r;
-          *reinterpret_cast<uint64_t*>(pl + GQ + o) = vmul(a.ay, grv).r;
+          if (NF == 2) *reinterpret_cast<uint64_t*>(pl + GQ + o) = vmul(a.ay, grv).r;
         }
         if (ROLE != 1) {  // a_z g: tapped along z (tile rows and z-halo columns)
-          *reinterpret_cast<uint64_t*>(pl + 2 * GQ + o) = vmul(a.az, gp).r;
-          *reinterpret_cast<uint64_t*>(pl + 3 * GQ + o) = vmul(a.az, grv).r;
+          *reinterpret_cast<uint64_t*>(pl + NF * GQ + o) = vmul(a.az, gp).r;
+          if (NF == 2) *reinterpret_cast<uint64_t*>(pl + 3 * GQ + o) = vmul(a.az, grv).r;
         }
         if constexpr (ROLE == 0) {
           const V2 axp = vmul(a.ax, gp), axr = vmul(a.ax, grv);
@@ -237,9 +247,9 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
             const int jj = R - k;
             const float cj = jj > 0 ? P.c.d1[0][jj] : -P.c.d1[0][-jj];
             accp[k] = vcfma(cj, axp, accp[k]);
-            accr[k] = vcfma(cj, axr, accr[k]);
+            if (NF == 2) accr[k] = vcfma(cj, axr, accr[k]);
           }
-          lapv = lap_point<R>(a, P.c);
+          if (NF == 2) lapv = lap_point<R>(a, P.c);
         }
       }
     }
@@ -249,31 +259,44 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
       if (gpl) {
         // (d) y / z parts of the outer derivative at x', folded at j = 0
         const float* q = pl + gr[0] * L::GZ + gc;
-        const V2 yzp = vadd(dplane<R, 1>(q, P.c.d1[1]), dplane<R, 2>(q + 2 * GQ, P.c.d1[2]));
-        const V2 yzr = vadd(dplane<R, 1>(q + GQ, P.c.d1[1]), dplane<R, 2>(q + 3 * GQ, P.c.d1[2]));
-        accp[R] = vadd(accp[R], vsub(yzp, lapv));
-        accr[R] = vadd(accr[R], yzr);
+        const V2 yzp = vadd(dplane<R, 1>(q, P.c.d1[1]), dplane<R, 2>(q + NF * GQ, P.c.d1[2]));
+        if constexpr (NF == 2) {
+          const V2 yzr = vadd(dplane<R, 1>(q + GQ, P.c.d1[1]),
+                              dplane<R, 2>(q + 3 * GQ, P.c.d1[2]));
+          accp[R] = vadd(accp[R], vsub(yzp, lapv));
+          accr[R] = vadd(accr[R], yzr);
+        } else {
+          accp[R] = vadd(accp[R], yzp);
+        }
         // (e) output x' - R is complete
         if (i >= 4 * R && (m0 || m1)) {
           const int x = xa - 4 * R + i;
           const float* pt = reinterpret_cast<const float*>(st + L::O_PT) + warp * kFTZ + 2 * lane;
           constexpr int PQ = L::PTB / 4;
-          V2 p1, r1;
-          fused_finish(P.c, vneg(accp[0]), accr[0], wp[0][0], wr[0][0], vload<2>(pt),
-                       vload<2>(pt + PQ), vload<2>(pt + 2 * PQ), vload<2>(pt + 3 * PQ),
-                       vload<2>(pt + 4 * PQ), p1, r1);
           const int64_t idx = (int64_t)x * g.sx + (int64_t)y * g.sy + z;
-          vstore(P.out[0], idx, p1, m0, m1);
-          vstore(P.out[1], idx, r1, m0, m1);
-          if (push.ndir) {
-            const V2 o2[2] = {p1, r1};
-            push_vals(push, x, y, z, o2, 2, m0, m1);
+          if constexpr (NF == 2) {
+            V2 p1, r1;
+            fused_finish(P.c, vneg(accp[0]), accr[0], wp[0][0], wr[0][0], vload<2>(pt),
+                         vload<2>(pt + PQ), vload<2>(pt + 2 * PQ), vload<2>(pt + 3 * PQ),
+                         vload<2>(pt + 4 * PQ), p1, r1);
+            vstore(P.out[0], idx, p1, m0, m1);
+            vstore(P.out[1], idx, r1, m0, m1);
+            if (push.ndir) {
+              const V2 o2[2] = {p1, r1};
+              push_vals(push, x, y, z, o2, 2, m0, m1);
+            }
+          } else {
+            // rot_point's tail: u1 = 2 u0 - u2 + dt^2/m G
+            const V2 ut = vfma(v2bcast(2.f), wp[0][0], vnegz(vload<2>(pt)));
+            const V2 u1 = vfma(vdiv(v2bcast(P.c.dt2), vload<2>(pt + PQ)), accp[0], ut);
+            vstore(P.out[0], idx, u1, m0, m1);
+            if (push.ndir) push_vals(push, x, y, z, &u1, 1, m0, m1);
           }
         }
 #pragma unroll
         for (int k = 0; k < W - 1; ++k) {
           accp[k] = accp[k + 1];
-          accr[k] = accr[k + 1];
+          if (NF == 2) accr[k] = accr[k + 1];
         }
         accp[W - 1] = accr[W - 1] = v2bcast(0.f);
       }
@@ -283,12 +306,11 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
   }
 }
 
-template <int R>
-__global__ void __launch_bounds__(FLayout<R>::THREADS, 1)
+template <int R, int NF>
+__global__ void __launch_bounds__(FLayout<R, NF>::THREADS, 1)
 tti_fused(const __grid_constant__ TMaps maps, const FusedTTI P, const int xchunk,
           const __grid_constant__ Push push) {
-  using L = FLayout<R>;
-  constexpr int W = 2 * R + 1;
+  using L = FLayout<R, NF>;
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = smraw;
   unsigned char* plane = sm + L::S * L::STAGE;
@@ -320,34 +342,41 @@ tti_fused(const __grid_constant__ TMaps maps, const FusedTTI P, const int xchunk
         const bool gpl = i >= 2 * R, upl = i >= 4 * R;
         mbar_arrive_expect_tx(&full_bar[s], L::TX_FRONT + (gpl ? L::TX_G : 0u) +
                                                 (upl ? L::TX_PT : 0u));
-        tma_load_3d(st + L::O_FP, &maps.m[0], &full_bar[s], z0 - L::OFF, y0 - R, xf);
-        tma_load_3d(st + L::O_FR, &maps.m[1], &full_bar[s], z0 - L::OFF, y0 - R, xf);
+        // maps: fronts [0, NF), centres [NF, 2NF), a [2NF, 2NF+3), points after
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+          tma_load_3d(st + L::O_FP + f * L::GREG, &maps.m[f], &full_bar[s], z0 - L::OFF, y0 - R,
+                      xf);
         if (gpl) {
-          tma_load_3d(st + L::O_CP, &maps.m[2], &full_bar[s], z0 - 2 * L::OFF, y0 - 2 * R, xf - R);
-          tma_load_3d(st + L::O_CR, &maps.m[3], &full_bar[s], z0 - 2 * L::OFF, y0 - 2 * R, xf - R);
+#pragma unroll
+          for (int f = 0; f < NF; ++f)
+            tma_load_3d(st + L::O_CP + f * L::CEN, &maps.m[NF + f], &full_bar[s],
+                        z0 - 2 * L::OFF, y0 - 2 * R, xf - R);
 #pragma unroll
           for (int q = 0; q < 3; ++q)
-            tma_load_3d(st + L::O_A + q * L::GREG, &maps.m[4 + q], &full_bar[s], z0 - L::OFF,
-                        y0 - R, xf - R);
+            tma_load_3d(st + L::O_A + q * L::GREG, &maps.m[2 * NF + q], &full_bar[s],
+                        z0 - L::OFF, y0 - R, xf - R);
         }
         if (upl) {
 #pragma unroll
-          for (int q = 0; q < 5; ++q)
-            tma_load_3d(st + L::O_PT + q * L::PTB, &maps.m[7 + q], &full_bar[s], z0, y0,
-                        xf - 2 * R);
+          for (int q = 0; q < L::NPT; ++q)
+            tma_load_3d(st + L::O_PT + q * L::PTB, &maps.m[2 * NF + 3 + q], &full_bar[s], z0,
+                        y0, xf - 2 * R);
         }
       }
     }
     return;
   }
-
   // consumers: one loop per role (separate register allocations)
   if (warp < kFTY)
-    fused_consumer<R, 0>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp, lane);
+    fused_consumer<R, 0, NF>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp,
+                             lane);
   else if (warp < kFTY + L::NHW)
-    fused_consumer<R, 1>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp, lane);
+    fused_consumer<R, 1, NF>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp,
+                             lane);
   else
-    fused_consumer<R, 2>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp, lane);
+    fused_consumer<R, 2, NF>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp,
+                             lane);
 }
 
 // ---- generic twin: one thread per output point, same order ------------------
@@ -414,26 +443,68 @@ __global__ void __launch_bounds__(256) tti_fused_generic(TTIGeneric p, const Pus
   }
 }
 
-// host: fused launch (TMA maps over the ten inputs)
+// single-field twin (rotated operator): same order with one accumulator, no
+// Laplacian, rot_point's update tail
 template <int R>
+__global__ void __launch_bounds__(256) rot_fused_generic(TTIGeneric p, const Push push) {
+  const int z = p.g.lo[2] + blockIdx.x * 32 + threadIdx.x;
+  const int y = p.g.lo[1] + blockIdx.y * 8 + threadIdx.y;
+  const int x = p.g.lo[0] + blockIdx.z;
+  if (z >= p.g.hi[2] || y >= p.g.hi[1]) return;
+  const int64_t sx = p.g.sx, sy = p.g.sy;
+  const int64_t i = x * sx + y * sy + z;
+  auto qprod = [&](int64_t j, int q) {  // RN(a_q g) at index j
+    TTIGlobalAcc a{p.tap, p.pnt, j, {sx, sy, 1}};
+    return __fmul_rn(__ldg(p.pnt[QAX + q] + j), g1_point<R>(a, p.c));
+  };
+  float acc = 0.f;
+#pragma unroll 1
+  for (int jj = -R; jj <= R; ++jj) {
+    if (jj == 0) {
+      float dy = 0.f, dz = 0.f;
+#pragma unroll 1
+      for (int k = 1; k <= R; ++k) {
+        dy = __fmaf_rn(p.c.d1[1][k], __fsub_rn(qprod(i + k * sy, 1), qprod(i - k * sy, 1)), dy);
+        dz = __fmaf_rn(p.c.d1[2][k], __fsub_rn(qprod(i + k, 2), qprod(i - k, 2)), dz);
+      }
+      acc = __fadd_rn(acc, __fadd_rn(dy, dz));
+    } else {
+      const float cj = jj > 0 ? p.c.d1[0][jj] : -p.c.d1[0][-jj];
+      acc = __fmaf_rn(cj, qprod(i + jj * sx, 0), acc);
+    }
+  }
+  const float ut = __fmaf_rn(2.f, __ldg(p.pnt[QR0] + i), __fsub_rn(0.f, __ldg(p.pnt[QP2] + i)));
+  const float v = __fmaf_rn(__fdiv_rn(p.c.dt2, __ldg(p.pnt[QM] + i)), acc, ut);
+  p.out[0][i] = v;
+  if (push.ndir) push_point(push, x, y, z, &v, 1);
+}
+
+// host: fused launch.  NF = 2 (TTI): maps {p, r | p, r | ax, ay, az | p2, r2,
+// m, epsp, delp}; NF = 1 (rotated): {u0 | u0 | ax, ay, az | u2, m}
+template <int R, int NF>
 static int launch_fused(const TTIGeneric& p, cudaStream_t st, const int64_t full[3],
                         const Push& push) {
-  using L = FLayout<R>;
+  using L = FLayout<R, NF>;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    SDMP_CUDA(cudaFuncSetAttribute(tti_fused<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SDMP_CUDA(cudaFuncSetAttribute(tti_fused<R, NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    L::BYTES));
     attr_dev = dev;
   }
   TMaps maps;
-  const float* src[12] = {p.tap[TP], p.tap[TR], p.tap[TP], p.tap[TR], p.pnt[QAX], p.pnt[QAY],
-                          p.pnt[QAZ], p.pnt[QP2], p.pnt[QR2], p.pnt[QM], p.pnt[QE], p.pnt[QD]};
-  for (int k = 0; k < 12; ++k) {
-    const int bz = k < 2 ? L::GZ : k < 4 ? L::CZ : k < 7 ? L::GZ : kFTZ;
-    const int by = k < 2 ? L::GY : k < 4 ? L::CY : k < 7 ? L::GY : kFTY;
-    int rc = make_tmap_3d(&maps.m[k], src[k], full, bz, by, k >= 7);
+  const float* src2[12] = {p.tap[TP], p.tap[TR], p.tap[TP], p.tap[TR], p.pnt[QAX], p.pnt[QAY],
+                           p.pnt[QAZ], p.pnt[QP2], p.pnt[QR2], p.pnt[QM], p.pnt[QE], p.pnt[QD]};
+  const float* src1[7] = {p.tap[TP], p.tap[TP], p.pnt[QAX], p.pnt[QAY], p.pnt[QAZ],
+                          p.pnt[QP2], p.pnt[QM]};
+  const float* const* src = NF == 2 ? src2 : src1;
+  constexpr int NMAP = 2 * NF + 3 + L::NPT;
+  for (int k = 0; k < NMAP; ++k) {
+    const bool front = k < NF, cen = k >= NF && k < 2 * NF, am = k >= 2 * NF && k < 2 * NF + 3;
+    const int bz = front || am ? L::GZ : cen ? L::CZ : kFTZ;
+    const int by = front || am ? L::GY : cen ? L::CY : kFTY;
+    int rc = make_tmap_3d(&maps.m[k], src[k], full, bz, by, k >= 2 * NF + 3);
     if (rc) return rc;
   }
   FusedTTI f{};
@@ -448,7 +519,7 @@ static int launch_fused(const TTIGeneric& p, cudaStream_t st, const int64_t full
   nch = (nx + chunk - 1) / chunk;
   SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");
   dim3 grid(tz, ty, nch), block(32, L::NCW + 1);
-  tti_fused<R><<<grid, block, L::BYTES, st>>>(maps, f, chunk, push);
+  tti_fused<R, NF><<<grid, block, L::BYTES, st>>>(maps, f, chunk, push);
   SDMP_LAUNCHED();
   return SDMP_OK;
 }

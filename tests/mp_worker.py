@@ -157,6 +157,8 @@ def main():
     results = {}
     cases = [("acoustic", acoustic, {}), ("diffusion", diffusion, {}), ("damped", damped, {}),
              ("rotated", rotated, {}), ("tti", tti, {}),
+             # SO-4: the single-pass kernels (csrc/tti_fused.cuh)
+             ("rotated4", rotated, {"so": 4}), ("tti4", tti, {"so": 4}),
              ("elastic", elastic, {}), ("elastic_col", elastic, {"collocated": True}),
              ("visco", elastic, {"visco": True, "so": 16})]
     only = os.environ.get("FAMILIES")

@@ -172,7 +172,8 @@ def test_star_kernels_bitwise_equal_generic(so, monkeypatch):
     assert np.abs(outs[0][0]).max() > 0
 
 
-@pytest.mark.parametrize("family,so", [("tti", 8), ("tti", 12), ("tti", 16), ("elastic", 8),
+@pytest.mark.parametrize("family,so", [("tti", 4), ("tti", 8), ("tti", 12), ("tti", 16),
+                                       ("rotated", 4), ("rotated", 8), ("elastic", 8),
                                        ("elastic", 4), ("elastic", 16), ("visco", 16),
                                        ("visco", 8)])
 def test_stream_kernels_bitwise_equal_generic(family, so, monkeypatch):
@@ -189,6 +190,10 @@ def test_stream_kernels_bitwise_equal_generic(family, so, monkeypatch):
         if family == "tti":
             kd = KD.tti_model(grid, so=so)
             names = ("p", "r")
+            dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.2)))
+        elif family == "rotated":
+            kd = KD.rotated_model(grid, so=so, name=f"urb{so}_{variant}")
+            names = ("u", "u")
             dt = float(np.float32(KD.critical_dt(4.6, grid.spacing, 0.2)))
         else:
             kd = (KD.viscoelastic_model(grid, so=so) if family == "visco"

@@ -18,6 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 FAMILIES = [("acoustic", {}), ("diffusion", {}), ("damped", {}), ("rotated", {}), ("tti", {}),
+            ("rotated4", {"so": 4}), ("tti4", {"so": 4}),
             ("elastic", {}), ("elastic_col", {"collocated": True}),
             ("visco", {"visco": True, "so": 16})]
 
@@ -30,7 +31,8 @@ def test_guards_and_exterior_halo(fam, kw, mode, monkeypatch):
     from memcheck_util import check_fields
     from paper_2312_13094_b200 import Grid
     build = {"acoustic": W.acoustic, "diffusion": W.diffusion, "damped": W.damped,
-             "rotated": W.rotated, "tti": W.tti}.get(fam, W.elastic)
+             "rotated": W.rotated, "tti": W.tti, "rotated4": W.rotated,
+             "tti4": W.tti}.get(fam, W.elastic)
     shape = (40, 36, 44)   # TMA-streamed DOMAIN boxes plus generic edges
     g = Grid(shape, tuple(10.0 * (n - 1) for n in shape), comm="self")
     op, dt, fields, rec = build(g, f"mem_{fam}_{mode}", 14, **kw)

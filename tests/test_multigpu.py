@@ -24,7 +24,7 @@ torch = pytest.importorskip("torch")
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ALL = "acoustic,diffusion,damped,rotated,tti,elastic,elastic_col,visco"
+ALL = "acoustic,diffusion,damped,rotated,tti,rotated4,tti4,elastic,elastic_col,visco"
 
 
 def _env(nproc, **extra):

@@ -13,7 +13,8 @@ run() {  # N kernel so shape mode tag
   timeout 900 $L bench.py --gpus $N --kernel $1 --so $2 $shp --mode $4 --steps 20 --warmup 3 --no-cpu-baseline 2>$O/err_$5.log | tail -1 > $O/$5.json
   python - "$O/$5.json" "$5" >> $O/summary.txt <<'PY' || tail -3 $O/err_$5.log >> $O/summary.txt
 import json, sys
-d = json.load(open(sys.argv[1])); h = d.get("halo") or {}; nv = h.get("nvlink_counters_rank0") or {}
+d = json.load(open(sys.argv[1])); h = d.get("halo") or {}; nv = h.get("nvlink_counters_rank0")
+nv = nv if isinstance(nv, dict) else {}
 print(sys.argv[2], round(d["value"], 1), "GPts/s ms", round(d["ms_per_step"], 3), "frac",
       round(d["roofline"]["frac"], 3), "e2e", round(d["e2e"]["value"], 1), "exposed",
       round(h.get("exposed_frac", 0), 4), "sent MB", round(h.get("halo_bytes_sent_per_step_rank0", 0) / 1e6, 1),
