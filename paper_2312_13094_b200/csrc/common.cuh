@@ -99,6 +99,22 @@ __device__ __forceinline__ void push_point(const Push& P, int x, int y, int z, c
   }
 }
 
+// one box copy of a batched halo post (k_multi_copy)
+struct CopyMsg {
+  const float* src;
+  float* dst;
+  int64_t ssx, ssy, dsx, dsy, soff, doff;
+  int ex, ey, ez;
+};
+constexpr int kMaxCopyMsgs = 96;
+struct MultiCopy {
+  int n = 0;
+  int64_t rows = 0;
+  int64_t row0[kMaxCopyMsgs];
+  CopyMsg m[kMaxCopyMsgs];
+};
+int multi_copy(cudaStream_t st, const MultiCopy& mc);
+
 inline bool box_empty(const Geom& g) {
   return g.hi[0] <= g.lo[0] || g.hi[1] <= g.lo[1] || g.hi[2] <= g.lo[2];
 }

@@ -329,7 +329,7 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
       // already pushed by the fused compute kernels, copy only on the first
       // step of a run (nothing was pushed before it)
       const int64_t phase = I[2];
-      const int engine = (int)(I[4] & 1);
+      const int engine = (int)(I[4] & 3);  // 0 copy engines, 1 SM per box, 2 SM batched
       const bool pushed = (I[4] & 16) && time != p->run_time_m;
       const int64_t nmsg = pushed ? 0 : I[3];
       const int64_t* m = I + 5;
@@ -340,7 +340,30 @@ int run_action(sdmp_plan* p, const Action& a, int64_t time) {
         SDMP_CUDA(cudaEventRecord(p->ev_fork, st));
         for (int c = 0; c < fan; ++c) SDMP_CUDA(cudaStreamWaitEvent(p->cs[c], p->ev_fork, 0));
       }
-      for (int64_t q = 0; q < nmsg; ++q, m += 12) {
+      if (engine == 2) {
+        // one kernel moves every box of the post (k_multi_copy)
+        MultiCopy mc;
+        for (int64_t q = 0; q < nmsg; ++q, m += 12) {
+          SDMP_CHECK(mc.n < kMaxCopyMsgs, "too many messages for a batched post");
+          const int64_t* sf = p->fields[m[0]].full;
+          const int64_t* df = p->fields[m[2]].full;
+          CopyMsg& c = mc.m[mc.n];
+          c.src = resolve(p, m[0], m[1], time);
+          c.dst = resolve(p, m[2], m[1], time);
+          c.ssy = sf[2]; c.ssx = sf[1] * sf[2];
+          c.dsy = df[2]; c.dsx = df[1] * df[2];
+          c.soff = m[3] * c.ssx + m[4] * c.ssy + m[5];
+          c.doff = m[6] * c.dsx + m[7] * c.dsy + m[8];
+          c.ex = (int)m[9]; c.ey = (int)m[10]; c.ez = (int)m[11];
+          if (c.ex <= 0 || c.ey <= 0 || c.ez <= 0) continue;
+          mc.row0[mc.n] = mc.rows;
+          mc.rows += (int64_t)c.ex * c.ey;
+          ++mc.n;
+        }
+        int rc = multi_copy(st, mc);
+        if (rc) return rc;
+      }
+      for (int64_t q = 0; engine != 2 && q < nmsg; ++q, m += 12) {
         const float* src = resolve(p, m[0], m[1], time);
         float* dst = resolve(p, m[2], m[1], time);
         cudaStream_t cst = fan > 1 ? p->cs[q % fan] : st;

@@ -119,6 +119,47 @@ static int box_copy_kernel(cudaStream_t st, const BoxXfer& b) {
   return SDMP_OK;
 }
 
+// ---- batched halo copy: every message of one post in ONE kernel ------------
+// (diagonal / basic mode with SDMP_COPY_ENGINE=batch).  Rows (x, y) of all
+// boxes are flattened; each warp moves one z row per iteration with 16-byte
+// loads / peer stores when the row is 16-byte aligned on both sides (the
+// whole-z rows of the product always are), scalar otherwise.
+
+__global__ void __launch_bounds__(256) k_multi_copy(const __grid_constant__ MultiCopy mc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < mc.rows;
+       r += nwarps) {
+    int m = 0;
+    while (m + 1 < mc.n && mc.row0[m + 1] <= r) ++m;
+    const CopyMsg& c = mc.m[m];
+    const int64_t rr = r - mc.row0[m];
+    const int64_t x = rr / c.ey, y = rr - x * c.ey;
+    const float* s = c.src + c.soff + x * c.ssx + y * c.ssy;
+    float* d = c.dst + c.doff + x * c.dsx + y * c.dsy;
+    const int ez = c.ez;
+    if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0) {
+      const int n4 = ez >> 2;
+      const float4* s4 = reinterpret_cast<const float4*>(s);
+      float4* d4 = reinterpret_cast<float4*>(d);
+      for (int i = lane; i < n4; i += 32) d4[i] = __ldg(s4 + i);
+      for (int i = (n4 << 2) + lane; i < ez; i += 32) d[i] = s[i];
+    } else {
+      for (int i = lane; i < ez; i += 32) d[i] = s[i];
+    }
+  }
+}
+
+int multi_copy(cudaStream_t st, const MultiCopy& mc) {
+  if (mc.n <= 0 || mc.rows <= 0) return SDMP_OK;
+  int64_t blocks = (mc.rows + 7) / 8;
+  const int64_t cap = 2ll * num_sms();
+  if (blocks > cap) blocks = cap;
+  k_multi_copy<<<(unsigned)blocks, 256, 0, st>>>(mc);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
 int pack(cudaStream_t st, const float* field, const int64_t full[3], const int64_t lo[3],
          const int64_t hi[3], float* buf) {
   Geom g;

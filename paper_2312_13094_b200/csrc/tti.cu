@@ -546,7 +546,7 @@ int tti_update_entry(cudaStream_t st, const float* const in[10], float* p1, floa
 template <int R>
 static int launch_rot(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const Push& push) {
 #ifndef SDMP_ROT_FUSED_MAXR
-#define SDMP_ROT_FUSED_MAXR 2
+#define SDMP_ROT_FUSED_MAXR 3  // r04 A/B (512^3): SO-4 176 vs 121, SO-6 112 vs 109, SO-8 94 vs 107 GPts/s
 #endif
   if constexpr (R <= SDMP_ROT_FUSED_MAXR) {
     // single pass for the narrow stencils, as for TTI (tti_fused.cuh, NF = 1)

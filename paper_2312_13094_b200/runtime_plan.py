@@ -263,7 +263,7 @@ class NativeOperatorPlan:
     def _post_ints(self, a, fid, pfid, pflag, decomp, rank):
         # SDMP_COPY_ENGINE=sm: halo copies as SM kernels storing over NVLink
         # (default: copy engines, cudaMemcpy3DAsync)
-        eng = 1 if os.environ.get("SDMP_COPY_ENGINE", "ce") == "sm" else 0
+        eng = {"ce": 0, "sm": 1, "batch": 2}[os.environ.get("SDMP_COPY_ENGINE", "ce")]
         ints = [R.ACT["POST"], a.stream, a.phase, 0, (16 if a.pushed else 0) | eng]
         # z is never split: its halo (and padding) is exterior on every rank,
         # zero on sender and receiver alike, so each message ships whole

@@ -45,8 +45,8 @@ def _torchrun(nproc, port, script, env, timeout):
     return subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
 
 
-def _run(nproc, topo, shape, families, steps=10, timeout=1500, port=29517):
-    env = _env(nproc, TOPO=topo, SHAPE=shape, FAMILIES=families, STEPS=str(steps))
+def _run(nproc, topo, shape, families, steps=10, timeout=1500, port=29517, **extra):
+    env = _env(nproc, TOPO=topo, SHAPE=shape, FAMILIES=families, STEPS=str(steps), **extra)
     res = _torchrun(nproc, port, ("tests", "mp_worker.py"), env, timeout)
     out = res.stdout.strip().splitlines()
     rep = json.loads(out[-1]) if out and out[-1].startswith("{") else {}
@@ -103,6 +103,18 @@ def test_eight_ranks_4x2_layout():
     diagonal (xy-edge) neighbours -- up to 8 messages per rank per phase."""
     rc, rep, err = _run(8, "4,2,1", "64,44,32", ALL, steps=8, timeout=2400, port=29524)
     _check(rc, rep, err, ALL)
+
+
+@needs_gpu
+@pytest.mark.parametrize("engine", ["sm", "batch"])
+def test_halo_copy_engines(engine):
+    """The SM alternatives to the copy-engine posts (SDMP_COPY_ENGINE=sm: one
+    kernel per box; batch: one kernel per post for every field and
+    direction) give the same bits."""
+    fams = "acoustic,elastic,visco"
+    rc, rep, err = _run(4, "2,2,1", "44,40,32", fams, port=29525 + (engine == "batch"),
+                        SDMP_COPY_ENGINE=engine)
+    _check(rc, rep, err, fams)
 
 
 @needs_gpu
