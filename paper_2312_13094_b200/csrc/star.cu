@@ -154,6 +154,50 @@ __device__ __forceinline__ void star_ztaps(const StarParams& p, const float* zw,
   }
 }
 
+// z neighbourhood of a thread's 4 points (zw[0 .. 4 + 2 OFF), centred at OFF):
+// SDMP_ZSHFL = 1 takes the thread's own 4 values from its x-window register
+// (the centre plane) and the neighbours' from the adjacent lanes' registers
+// by warp shuffles; only lanes at the warp's edge read the staged halo
+// columns.  0 reads the whole neighbourhood from the staged centre row
+// (NZW 16-byte loads).  Same values either way.  All 32 lanes must call it.
+#ifndef SDMP_ZSHFL
+#define SDMP_ZSHFL 0
+#endif
+template <int OFF>
+__device__ __forceinline__ void star_zwin(float* zw, const float4& own, const float* row,
+                                          int lane) {
+  constexpr int NZW = (4 + 2 * OFF) / 4;
+#if SDMP_ZSHFL
+  zw[OFF + 0] = own.x; zw[OFF + 1] = own.y; zw[OFF + 2] = own.z; zw[OFF + 3] = own.w;
+#pragma unroll
+  for (int t = 1; t <= OFF / 4; ++t) {
+    float4 lo, hi;
+    lo.x = __shfl_up_sync(0xffffffffu, own.x, t);
+    lo.y = __shfl_up_sync(0xffffffffu, own.y, t);
+    lo.z = __shfl_up_sync(0xffffffffu, own.z, t);
+    lo.w = __shfl_up_sync(0xffffffffu, own.w, t);
+    hi.x = __shfl_down_sync(0xffffffffu, own.x, t);
+    hi.y = __shfl_down_sync(0xffffffffu, own.y, t);
+    hi.z = __shfl_down_sync(0xffffffffu, own.z, t);
+    hi.w = __shfl_down_sync(0xffffffffu, own.w, t);
+    if (lane < t) lo = *reinterpret_cast<const float4*>(row - 4 * t);
+    if (lane + t > 31) hi = *reinterpret_cast<const float4*>(row + 4 * t);
+    const int l0 = OFF - 4 * t, h0 = OFF + 4 * t;
+    zw[l0 + 0] = lo.x; zw[l0 + 1] = lo.y; zw[l0 + 2] = lo.z; zw[l0 + 3] = lo.w;
+    zw[h0 + 0] = hi.x; zw[h0 + 1] = hi.y; zw[h0 + 2] = hi.z; zw[h0 + 3] = hi.w;
+  }
+  (void)NZW;
+#else
+  (void)own;
+  (void)lane;
+#pragma unroll
+  for (int q = 0; q < NZW; ++q) {
+    const float4 v = *reinterpret_cast<const float4*>(row - OFF + 4 * q);
+    zw[4 * q + 0] = v.x; zw[4 * q + 1] = v.y; zw[4 * q + 2] = v.z; zw[4 * q + 3] = v.w;
+  }
+#endif
+}
+
 // u1 = A u0 + B u2 + S lap on 4 points (star_finish per lane)
 __device__ __forceinline__ void star_finish4(const StarParams& p, const V2 lap[2], const float4& c0,
                                              const float4& u2v, const float4& mv, float out[4]) {
@@ -291,19 +335,16 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
 
   // one pipeline iteration; the x-window plane of logical index kk (0 =
   // oldest, 2R = newest) sits in register slot (rot + kk + 1) % W
+  const bool yact = y < p.g.hi[1];  // warp-uniform (one row per warp)
   auto consume = [&](int i, int rot, const unsigned char* st) {
     auto wv = [&](int kk) -> const float4& { return w[(rot + kk + 1) % W]; };
-    if (i >= 2 * R && active) {
+    if (i >= 2 * R && yact) {  // every lane of the warp (shuffles), stores masked
       const int x = xa + i - 2 * R;
       const float* row = reinterpret_cast<const float*>(st + T::FRONT) + (warp + R) * T::CZ +
                          T::OFF + 4 * lane;
       constexpr int NZW = (4 + 2 * T::OFF) / 4;
       float zw[4 * NZW];
-#pragma unroll
-      for (int q = 0; q < NZW; ++q) {
-        float4 v = *reinterpret_cast<const float4*>(row - T::OFF + 4 * q);
-        zw[4 * q + 0] = v.x; zw[4 * q + 1] = v.y; zw[4 * q + 2] = v.z; zw[4 * q + 3] = v.w;
-      }
+      star_zwin<T::OFF>(zw, wv(R), row, lane);
       float4 u2v = make_float4(0.f, 0.f, 0.f, 0.f), mv = make_float4(1.f, 1.f, 1.f, 1.f);
       if (has_u2)
         u2v = *reinterpret_cast<const float4*>(
@@ -334,7 +375,7 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
       star_ztaps<R, T::OFF>(p, zw, lap);
       float out[4];
       star_finish4(p, lap, wv(R), u2v, mv, out);
-      star_store4(p, push, x, y, z, out);
+      if (active) star_store4(p, push, x, y, z, out);
     }
   };
 
@@ -499,8 +540,9 @@ star_tma2(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ 
   for (int k = 0; k < W + U - 1; ++k) w0[k] = w1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
 
   // one x-plane: window slots b .. b + 2R (b = group position, a constant)
+  const bool ract = y0 + r0 < p.g.hi[1];  // warp-uniform: the warp's first row
   auto consume = [&](const int i, const int b, const unsigned char* st) {
-    if (i >= 2 * R && (act0 || act1)) {
+    if (i >= 2 * R && ract) {  // every lane of the warp (shuffles), stores masked
       const int x = xa + i - 2 * R;
       // centre tile row (r0 + R + d) at this thread's 4 z points
       const float* crow = reinterpret_cast<const float*>(st + T::FRONT) + (r0 + R) * T::CZ +
@@ -541,12 +583,7 @@ star_tma2(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ 
       const float* pts = reinterpret_cast<const float*>(st + T::FRONT + T::CENTER) + 4 * lane;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const float* zr = crow + j * T::CZ - T::OFF;
-#pragma unroll
-        for (int q = 0; q < NZW; ++q) {
-          const float4 v = *reinterpret_cast<const float4*>(zr + 4 * q);
-          zw[4 * q + 0] = v.x; zw[4 * q + 1] = v.y; zw[4 * q + 2] = v.z; zw[4 * q + 3] = v.w;
-        }
+        star_zwin<T::OFF>(zw, j == 0 ? w0[b + R] : w1[b + R], crow + j * T::CZ, lane);
         V2* l = j == 0 ? l0 : l1;
         star_ztaps<R, T::OFF>(p, zw, l);
         const int rr = r0 + j;

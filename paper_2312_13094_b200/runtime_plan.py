@@ -261,9 +261,12 @@ class NativeOperatorPlan:
         return ints
 
     def _post_ints(self, a, fid, pfid, pflag, decomp, rank):
-        # SDMP_COPY_ENGINE=sm: halo copies as SM kernels storing over NVLink
-        # (default: copy engines, cudaMemcpy3DAsync)
-        eng = {"ce": 0, "sm": 1, "batch": 2}[os.environ.get("SDMP_COPY_ENGINE", "ce")]
+        # halo copies of diagonal / basic posts: one SM kernel storing every
+        # box of the post over NVLink (default, "batch"; r04 A/B on 2 GPUs:
+        # elastic diagonal 572 vs 517 GB/s, exposed 2.5% vs 2.9-4.4%), copy
+        # engines ("ce", cudaMemcpy3DAsync on 4 streams) or one SM kernel per
+        # box ("sm")
+        eng = {"ce": 0, "sm": 1, "batch": 2}[os.environ.get("SDMP_COPY_ENGINE", "batch")]
         ints = [R.ACT["POST"], a.stream, a.phase, 0, (16 if a.pushed else 0) | eng]
         # z is never split: its halo (and padding) is exterior on every rank,
         # zero on sender and receiver alike, so each message ships whole

@@ -106,13 +106,13 @@ def test_eight_ranks_4x2_layout():
 
 
 @needs_gpu
-@pytest.mark.parametrize("engine", ["sm", "batch"])
+@pytest.mark.parametrize("engine", ["sm", "ce"])
 def test_halo_copy_engines(engine):
-    """The SM alternatives to the copy-engine posts (SDMP_COPY_ENGINE=sm: one
-    kernel per box; batch: one kernel per post for every field and
-    direction) give the same bits."""
+    """The alternatives to the default batched SM posts (SDMP_COPY_ENGINE=sm:
+    one kernel per box; ce: copy engines, cudaMemcpy3DAsync) give the same
+    bits."""
     fams = "acoustic,elastic,visco"
-    rc, rep, err = _run(4, "2,2,1", "44,40,32", fams, port=29525 + (engine == "batch"),
+    rc, rep, err = _run(4, "2,2,1", "44,40,32", fams, port=29525 + (engine == "ce"),
                         SDMP_COPY_ENGINE=engine)
     _check(rc, rep, err, fams)
 
