@@ -87,7 +87,9 @@ int sdmp_bind_scale(void* stream, float* out, const float* in, int64_t n, float 
 /* Pseudo-acoustic TTI (SPEC.md:594-601 nested D^T D):
  * in[] = {p0, p2, r0, r2, m, epsp, delp, ax, ay, az}; out p1, r1.
  * lap_c, d1_c: 3 * SDMP_NCOEF (d1_c[a*NCOEF + k] = w1_k / h_a, k >= 1).
- * Reads p0/r0 up to 2*radius (= SO) from each point, ax/ay/az up to radius. */
+ * Reads p0/r0 up to 2*radius (= SO) from each point, ax/ay/az up to radius.
+ * radius | SDMP_VARIANT_M_IS_SCALE: the m operand holds the bound scale
+ * dt2/m (sdmp_bind_scale) instead of m (same results). */
 int sdmp_tti_update(void* stream, const float* const in[10], float* p1, float* r1,
                     const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
                     int32_t radius, const float* lap_c, const float* d1_c, float dt2,
@@ -96,7 +98,8 @@ int sdmp_tti_update(void* stream, const float* const in[10], float* p1, float* r
 /* Single-field rotated operator (the SPEC's tti_gxx_kernel):
  * m u_tt = G u with G u = sum_i D_i(a_i sum_j a_j D_j u) (nested centred first
  * derivatives), solved u1 = 2 u0 - u2 + dt2/m G u0.  in[] = {u0, u2, m, ax,
- * ay, az}; d1_c as for sdmp_tti_update; reads u0 up to 2*radius. */
+ * ay, az}; d1_c as for sdmp_tti_update; reads u0 up to 2*radius;
+ * radius | SDMP_VARIANT_M_IS_SCALE as for sdmp_tti_update. */
 int sdmp_rot_update(void* stream, const float* const in[6], float* u1, const int64_t full[3],
                     const int64_t lo[3], const int64_t hi[3], int32_t radius,
                     const float* d1_c, float dt2);

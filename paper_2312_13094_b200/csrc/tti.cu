@@ -31,7 +31,14 @@ struct TTICoef {
   float d1[3][SDMP_NCOEF];
   float csum0;
   float dt2;
+  int m_is_scale;  // the m operand already holds RN(dt2 / m) (bound by the plan)
 };
+
+// dt2 / m per point, or the bound scale (identical bits: __fdiv_rn both ways)
+template <class T>
+__device__ __forceinline__ T tti_scale(const TTICoef& c, T m) {
+  return c.m_is_scale ? m : vdiv(vconst<T>(c.dt2), m);
+}
 
 // logical ids: tap fields and pointwise fields
 enum { TP = 0, TR, TAX, TAY, TAZ, TGP, TGR, NT_ };
@@ -100,7 +107,7 @@ __device__ __forceinline__ void u_point(const A& a, const TTICoef& c, typename A
   for (int k = 1; k <= R; ++k)
     lap = vcfma(c.lap[2][k], vadd(a.template t<TP, 2>(-k), a.template t<TP, 2>(k)), lap);
   const T h0 = vsub(lap, gzp);
-  const T sc = vdiv(vconst<T>(c.dt2), a.template q<QM>());
+  const T sc = tti_scale(c, a.template q<QM>());
   const T e = a.template q<QE>(), d = a.template q<QD>();
   const T pp = vfma(d, gzr, vmul(e, h0));
   const T rr = vfma(d, h0, gzr);
@@ -131,7 +138,7 @@ __device__ __forceinline__ typename A::T rot_point(const A& a, const TTICoef& c)
   T G = outer<R, 0, TAX, TGP>(a, c.d1[0]);
   G = vadd(G, outer<R, 1, TAY, TGP>(a, c.d1[1]));
   G = vadd(G, outer<R, 2, TAZ, TGP>(a, c.d1[2]));
-  const T sc = vdiv(vconst<T>(c.dt2), a.template q<QM>());
+  const T sc = tti_scale(c, a.template q<QM>());
   const T ut = vfma(vconst<T>(2.f), a.template q<QR0>(), vnegz(a.template q<QP2>()));
   return vfma(sc, G, ut);
 }
@@ -494,6 +501,8 @@ int tti_update_entry(cudaStream_t st, const float* const in[10], float* p1, floa
                      const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
                      int32_t radius, const float* lap_c, const float* d1_c, float dt2,
                      const Push* push_in) {
+  const int m_is_scale = (radius & SDMP_VARIANT_M_IS_SCALE) ? 1 : 0;
+  radius &= 0xff;
   const Push nopush{};
   const Push& push = push_in ? *push_in : nopush;
   TTIGeneric p{};
@@ -529,6 +538,7 @@ int tti_update_entry(cudaStream_t st, const float* const in[10], float* p1, floa
   }
   p.c.csum0 = cs;
   p.c.dt2 = dt2;
+  p.c.m_is_scale = m_is_scale;
   switch (radius) {
     case 1: return launch<1>(p, st, full, push);
     case 2: return launch<2>(p, st, full, push);
@@ -617,6 +627,8 @@ static int launch_rot(TTIGeneric& p, cudaStream_t st, const int64_t full[3], con
 int rot_update_entry(cudaStream_t st, const float* const in[6], float* u1,
                      const int64_t full[3], const int64_t lo[3], const int64_t hi[3],
                      int32_t radius, const float* d1_c, float dt2, const Push* push_in) {
+  const int m_is_scale = (radius & SDMP_VARIANT_M_IS_SCALE) ? 1 : 0;
+  radius &= 0xff;
   const Push nopush{};
   const Push& push = push_in ? *push_in : nopush;
   TTIGeneric p{};
@@ -644,6 +656,7 @@ int rot_update_entry(cudaStream_t st, const float* const in[6], float* u1,
     for (int k = 0; k < SDMP_NCOEF; ++k)
       p.c.d1[a][k] = (k >= 1 && k <= radius) ? d1_c[a * SDMP_NCOEF + k] : 0.f;
   p.c.dt2 = dt2;
+  p.c.m_is_scale = m_is_scale;
   switch (radius) {
     case 1: return launch_rot<1>(p, st, full, push);
     case 2: return launch_rot<2>(p, st, full, push);

@@ -119,7 +119,7 @@ __device__ __forceinline__ typename A::T lap_point(const A& a, const TTICoef& c)
 template <class T>
 __device__ __forceinline__ void fused_finish(const TTICoef& c, T h0, T gzr, T p0, T r0, T p2,
                                              T r2, T m, T e, T d, T& p1, T& r1) {
-  const T sc = vdiv(vconst<T>(c.dt2), m);
+  const T sc = tti_scale(c, m);
   const T pp = vfma(d, gzr, vmul(e, h0));
   const T rr = vfma(d, h0, gzr);
   const T two = vconst<T>(2.f);
@@ -288,7 +288,7 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
           } else {
             // rot_point's tail: u1 = 2 u0 - u2 + dt^2/m G
             const V2 ut = vfma(v2bcast(2.f), wp[0][0], vnegz(vload<2>(pt)));
-            const V2 u1 = vfma(vdiv(v2bcast(P.c.dt2), vload<2>(pt + PQ)), accp[0], ut);
+            const V2 u1 = vfma(tti_scale(P.c, vload<2>(pt + PQ)), accp[0], ut);
             vstore(P.out[0], idx, u1, m0, m1);
             if (push.ndir) push_vals(push, x, y, z, &u1, 1, m0, m1);
           }
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(256) rot_fused_generic(TTIGeneric p, const Pus
     }
   }
   const float ut = __fmaf_rn(2.f, __ldg(p.pnt[QR0] + i), __fsub_rn(0.f, __ldg(p.pnt[QP2] + i)));
-  const float v = __fmaf_rn(__fdiv_rn(p.c.dt2, __ldg(p.pnt[QM] + i)), acc, ut);
+  const float v = __fmaf_rn(tti_scale(p.c, __ldg(p.pnt[QM] + i)), acc, ut);
   p.out[0][i] = v;
   if (push.ndir) push_point(push, x, y, z, &v, 1);
 }

@@ -173,13 +173,14 @@ class NativeOperatorPlan:
                 r = k.so // 2
                 w1 = [float(c) for c in S.fd_coefficients(1, k.so)]
                 d1 = [[0.0] + [_f32(w1[r + j] / h) for j in range(1, r + 1)] for h in spacing]
-                self.kparams[id(k)] = (list(R.coeff_table(d1, R.SDMP_NCOEF).ravel()) +
-                                       [_f32(float(dt) * float(dt))],)
+                dt2 = _f32(float(dt) * float(dt))
+                self.kparams[id(k)] = (list(R.coeff_table(d1, R.SDMP_NCOEF).ravel()) + [dt2],
+                                       self._bound_scale(op.fields[k.m], dt2))
             elif isinstance(k, CP.TTIKernel):
                 lap, d1, dt2 = tti_binding(k, spacing, dt)
                 fl = list(R.coeff_table(lap, R.SDMP_NCOEF).ravel()) + \
                     list(R.coeff_table(d1, R.SDMP_NCOEF).ravel()) + [dt2]
-                self.kparams[id(k)] = (fl,)
+                self.kparams[id(k)] = (fl, self._bound_scale(op.fields[k.m], dt2))
             elif isinstance(k, CP.StaggeredPhase):
                 sc, dtf = staggered_binding(k, spacing, dt)
                 self.kparams[id(k)] = (list(R.coeff_table(sc, R.SDMP_MAX_RADIUS).ravel()) + [dtf],)
@@ -200,6 +201,16 @@ class NativeOperatorPlan:
         self.plan.set_graph(os.environ.get("SDMP_GRAPH", "1") != "0")
 
     # ------------------------------------------------------------------
+    def _bound_scale(self, mfn, dt2):
+        """S = fp32(dt^2) / m bound once per static-field version (the
+        kernels read S instead of dividing per point; __fdiv_rn in both
+        places, so the bits are unchanged).  Returns S's plan field id."""
+        torch = __import__("torch")
+        sbuf = torch.zeros_like(mfn.storage[0])
+        self.scale_bufs.append((sbuf, mfn, dt2))
+        self.keep.append(sbuf)
+        return self.plan.add_field([int(sbuf.data_ptr())], mfn.full3)
+
     def _full_box(self, spec, box):
         fn = self.op.fields[spec]
         nd = len(box[0])
@@ -315,23 +326,24 @@ class NativeOperatorPlan:
                 lo + hi + r + [0]
             return ints, fl
         if isinstance(k, CP.RotatedKernel):
-            (fl,) = self.kparams[id(k)]
+            fl, sid = self.kparams[id(k)]
             lo, hi = self._full_box(k.u, box)
             refs = [(k.u, 0), (k.u, -1), (k.m, 0), (k.a[0], 0), (k.a[1], 0), (k.a[2], 0),
                     (k.u, 1)]
             ints = [R.ACT["ROT"], stream]
             for f, t in refs:
-                ints += [fid[f], t]
-            return ints + lo + hi + [k.so // 2], fl
+                ints += [sid if f == k.m else fid[f], t]
+            # radius | M_IS_SCALE: the m slot carries the bound dt^2/m
+            return ints + lo + hi + [(k.so // 2) | R.VARIANT_M_IS_SCALE], fl
         if isinstance(k, CP.TTIKernel):
-            (fl,) = self.kparams[id(k)]
+            fl, sid = self.kparams[id(k)]
             lo, hi = self._full_box(k.p, box)
             refs = [(k.p, 0), (k.p, -1), (k.r, 0), (k.r, -1), (k.m, 0), (k.epsp, 0),
                     (k.delp, 0), (k.a[0], 0), (k.a[1], 0), (k.a[2], 0), (k.p, 1), (k.r, 1)]
             ints = [R.ACT["TTI"], stream]
             for f, t in refs:
-                ints += [fid[f], t]
-            return ints + lo + hi + [k.so // 2], fl
+                ints += [sid if f == k.m else fid[f], t]
+            return ints + lo + hi + [(k.so // 2) | R.VARIANT_M_IS_SCALE], fl
         if isinstance(k, CP.StaggeredPhase):
             (fl,) = self.kparams[id(k)]
             lo, hi = self._full_box(k.v[0], box)
