@@ -438,12 +438,13 @@ static int variant_env() {
 template <int R>
 static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const Push& push) {
 #ifndef SDMP_TTI_FUSED_MAXR
-#define SDMP_TTI_FUSED_MAXR 2
+#define SDMP_TTI_FUSED_MAXR 3
 #endif
   if constexpr (R <= SDMP_TTI_FUSED_MAXR) {
-    // single pass (tti_fused.cuh) where it beats the two passes (r04, 512^3:
-    // SO-4 87.0 vs 70.1 GPts/s; SO-8 51.9 vs 65.8 -- at R = 4 the 2R halo
-    // rows double the g work of an 8-row tile); its
+    // single pass (tti_fused.cuh) where it beats the two passes (r04, 512^3,
+    // unrolled, bound dt^2/m: SO-4 92.7 vs 70.1 GPts/s, SO-6 74.5 vs 68.1;
+    // SO-8 49.5 vs 66.3 -- at R = 4 the 2R halo rows double the g work of
+    // an 8-row tile); its
     // generic twin for boxes the TMA loads cannot cover and for the bitwise
     // tests (SDMP_TTI_VARIANT=1)
     const float* in[10] = {p.tap[TP], p.pnt[QP2], p.tap[TR], p.pnt[QR2], p.pnt[QM],
@@ -556,7 +557,7 @@ int tti_update_entry(cudaStream_t st, const float* const in[10], float* p1, floa
 template <int R>
 static int launch_rot(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const Push& push) {
 #ifndef SDMP_ROT_FUSED_MAXR
-#define SDMP_ROT_FUSED_MAXR 3  // r04 A/B (512^3): SO-4 176 vs 121, SO-6 112 vs 109, SO-8 94 vs 107 GPts/s
+#define SDMP_ROT_FUSED_MAXR 4  // r04 A/B (512^3, unrolled, bound dt^2/m): SO-4 187 vs 121, SO-6 120 vs 109, SO-8 111 vs 106 GPts/s
 #endif
   if constexpr (R <= SDMP_ROT_FUSED_MAXR) {
     // single pass for the narrow stencils, as for TTI (tti_fused.cuh, NF = 1)

@@ -77,6 +77,7 @@ struct FAcc {
   using L = FLayout<R>;  // CZ does not depend on NF
   const V2 (&wp)[W];
   const V2 (&wr)[W];
+  int b;            // window slot of plane x' - R (a constant after unrolling)
   const float* cp;  // centre p at this pair (centre row / column already applied)
   const float* cr;
   V2 ax, ay, az;
@@ -90,7 +91,7 @@ struct FAcc {
   }
   template <int F, int AX>
   __device__ __forceinline__ V2 t(int k) const {
-    if (AX == 0) return F == TP ? wp[R + k] : wr[R + k];
+    if (AX == 0) return F == TP ? wp[b + R + k] : wr[b + R + k];
     const float* b = F == TP ? cp : cr;
     return AX == 1 ? tap(b, k, 0) : tap(b, 0, k);
   }
@@ -161,7 +162,6 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
   constexpr int W = 2 * R + 1;
   constexpr int NP = ROLE == 1 ? 2 : 1;  // point pairs of this thread
   constexpr int GQ = L::GREG / 4;
-  constexpr int NA = ROLE == 0 ? W : 1;
   const Geom& g = P.g;
   int gr[NP], gc;
   if (ROLE == 0) {
@@ -186,32 +186,36 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
   const bool m0 = yin && z >= g.lo[2] && z < g.hi[2];
   const bool m1 = yin && z + 1 >= g.lo[2] && z + 1 < g.hi[2];
 
-  V2 wp[NP][W], wr[NP][W];  // x-windows (planes x'-R .. x'+R after the load)
-  V2 accp[NA], accr[NA];    // outputs x'-R .. x'+R (tile role)
+  // x-windows and accumulators unrolled by U planes: inside a group the
+  // slots are constants (plane x'-R+k of sub-step u at slot u + k, output
+  // x'-R+k at accumulator u + k); the live entries move down once per group
+#ifndef SDMP_FUSED_UNROLL
+#define SDMP_FUSED_UNROLL 2
+#endif
+  constexpr int U = SDMP_FUSED_UNROLL;
+  constexpr int WB = W + U - 1;
+  constexpr int NA = ROLE == 0 ? WB : 1;
+  V2 wp[NP][WB], wr[NP][WB];
+  V2 accp[NA], accr[NA];
 #pragma unroll
-  for (int k = 0; k < W; ++k)
+  for (int k = 0; k < WB; ++k)
 #pragma unroll
     for (int j = 0; j < NP; ++j) wp[j][k] = wr[j][k] = v2bcast(0.f);
 #pragma unroll
   for (int k = 0; k < NA; ++k) accp[k] = accr[k] = v2bcast(0.f);
   V2 lapv = v2bcast(0.f);
 
-  for (int i = 0; i < nit; ++i) {
+  auto step = [&](const int i, const int u) {
     const int s = i % L::S;
     mbar_wait(&full_bar[s], (i / L::S) & 1);
     const unsigned char* st = sm + s * L::STAGE;
     float* pl = reinterpret_cast<float*>(plane + (i & 1) * L::PLANE);
-    // (a) x-windows
+    // (a) x-windows: plane x'+R lands in slot u + 2R
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
-#pragma unroll
-      for (int k = 0; k < W - 1; ++k) {
-        wp[j][k] = wp[j][k + 1];
-        if (NF == 2) wr[j][k] = wr[j][k + 1];
-      }
       const int o = gr[j] * L::GZ + gc;
-      wp[j][W - 1] = vload<2>(reinterpret_cast<const float*>(st + L::O_FP) + o);
-      if (NF == 2) wr[j][W - 1] = vload<2>(reinterpret_cast<const float*>(st + L::O_FR) + o);
+      wp[j][u + W - 1] = vload<2>(reinterpret_cast<const float*>(st + L::O_FP) + o);
+      if (NF == 2) wr[j][u + W - 1] = vload<2>(reinterpret_cast<const float*>(st + L::O_FR) + o);
     }
     const bool gpl = i >= 2 * R;
     // (b) g at this thread's points, product planes, x scatter, Laplacian
@@ -221,10 +225,10 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
         const int o = gr[j] * L::GZ + gc;
         const int oc = (gr[j] + R) * L::CZ + gc + L::OFF;
         const float* A = reinterpret_cast<const float*>(st + L::O_A);
-        FAcc<R, W> a{wp[j], NF == 2 ? wr[j] : wp[j],
-                     reinterpret_cast<const float*>(st + L::O_CP) + oc,
-                     reinterpret_cast<const float*>(st + L::O_CR) + oc, vload<2>(A + o),
-                     vload<2>(A + GQ + o), vload<2>(A + 2 * GQ + o)};
+        FAcc<R, WB> a{wp[j], NF == 2 ? wr[j] : wp[j], u,
+                      reinterpret_cast<const float*>(st + L::O_CP) + oc,
+                      reinterpret_cast<const float*>(st + L::O_CR) + oc, vload<2>(A + o),
+                      vload<2>(A + GQ + o), vload<2>(A + 2 * GQ + o)};
         V2 gp, grv = v2bcast(0.f);
         if constexpr (NF == 2)
           g_point<R>(a, P.c, gp, grv);
@@ -240,14 +244,14 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
         }
         if constexpr (ROLE == 0) {
           const V2 axp = vmul(a.ax, gp), axr = vmul(a.ax, grv);
-          // accumulator k holds output x' - R + k: plane x' is its x + (R - k)
+          // accumulator u + k holds output x' - R + k: plane x' is its x + (R - k)
 #pragma unroll
           for (int k = 0; k < W; ++k) {
             if (k == R) continue;
             const int jj = R - k;
             const float cj = jj > 0 ? P.c.d1[0][jj] : -P.c.d1[0][-jj];
-            accp[k] = vcfma(cj, axp, accp[k]);
-            if (NF == 2) accr[k] = vcfma(cj, axr, accr[k]);
+            accp[u + k] = vcfma(cj, axp, accp[u + k]);
+            if (NF == 2) accr[u + k] = vcfma(cj, axr, accr[u + k]);
           }
           if (NF == 2) lapv = lap_point<R>(a, P.c);
         }
@@ -263,10 +267,10 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
         if constexpr (NF == 2) {
           const V2 yzr = vadd(dplane<R, 1>(q + GQ, P.c.d1[1]),
                               dplane<R, 2>(q + 3 * GQ, P.c.d1[2]));
-          accp[R] = vadd(accp[R], vsub(yzp, lapv));
-          accr[R] = vadd(accr[R], yzr);
+          accp[u + R] = vadd(accp[u + R], vsub(yzp, lapv));
+          accr[u + R] = vadd(accr[u + R], yzr);
         } else {
-          accp[R] = vadd(accp[R], yzp);
+          accp[u + R] = vadd(accp[u + R], yzp);
         }
         // (e) output x' - R is complete
         if (i >= 4 * R && (m0 || m1)) {
@@ -276,7 +280,7 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
           const int64_t idx = (int64_t)x * g.sx + (int64_t)y * g.sy + z;
           if constexpr (NF == 2) {
             V2 p1, r1;
-            fused_finish(P.c, vneg(accp[0]), accr[0], wp[0][0], wr[0][0], vload<2>(pt),
+            fused_finish(P.c, vneg(accp[u]), accr[u], wp[0][u], wr[0][u], vload<2>(pt),
                          vload<2>(pt + PQ), vload<2>(pt + 2 * PQ), vload<2>(pt + 3 * PQ),
                          vload<2>(pt + 4 * PQ), p1, r1);
             vstore(P.out[0], idx, p1, m0, m1);
@@ -287,22 +291,39 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
             }
           } else {
             // rot_point's tail: u1 = 2 u0 - u2 + dt^2/m G
-            const V2 ut = vfma(v2bcast(2.f), wp[0][0], vnegz(vload<2>(pt)));
-            const V2 u1 = vfma(tti_scale(P.c, vload<2>(pt + PQ)), accp[0], ut);
+            const V2 ut = vfma(v2bcast(2.f), wp[0][u], vnegz(vload<2>(pt)));
+            const V2 u1 = vfma(tti_scale(P.c, vload<2>(pt + PQ)), accp[u], ut);
             vstore(P.out[0], idx, u1, m0, m1);
             if (push.ndir) push_vals(push, x, y, z, &u1, 1, m0, m1);
           }
         }
-#pragma unroll
-        for (int k = 0; k < W - 1; ++k) {
-          accp[k] = accp[k + 1];
-          if (NF == 2) accr[k] = accr[k + 1];
-        }
-        accp[W - 1] = accr[W - 1] = v2bcast(0.f);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
+  };
+
+  for (int i0 = 0; i0 < nit; i0 += U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u < nit) step(i0 + u, u);
+    // the W-1 newest planes / the pending outputs move down one group
+#pragma unroll
+    for (int k = 0; k < W - 1; ++k)
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        wp[j][k] = wp[j][k + U];
+        if (NF == 2) wr[j][k] = wr[j][k + U];
+      }
+    if constexpr (ROLE == 0) {
+#pragma unroll
+      for (int k = 0; k < W - 1; ++k) {
+        accp[k] = accp[k + U];
+        if (NF == 2) accr[k] = accr[k + U];
+      }
+#pragma unroll
+      for (int k = W - 1; k < WB; ++k) accp[k] = accr[k] = v2bcast(0.f);
+    }
   }
 }
 
