@@ -360,7 +360,10 @@ static int launch_el_stream(const Op& op, const Geom& g, const int64_t full[3],
 #endif
   constexpr bool vel = Op::NP <= 4, visco = Op::NP == 15;
   constexpr int V = (visco && R > 4) ? 1 : ((vel && R > 4) ? SDMP_VEL_VW : 2);
-  constexpr int TYN = vel ? SDMP_VEL_TYN : (visco ? 16 : 8);
+#ifndef SDMP_VISCO_TYN
+#define SDMP_VISCO_TYN 16
+#endif
+  constexpr int TYN = vel ? SDMP_VEL_TYN : (visco ? SDMP_VISCO_TYN : 8);
 #ifndef SDMP_STRESS_TYW
 #define SDMP_STRESS_TYW 8
 #endif

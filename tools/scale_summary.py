@@ -7,6 +7,8 @@ import sys
 d = sys.argv[1] if len(sys.argv) > 1 else "profiles/round2_scale"
 for f in sorted(glob.glob(os.path.join(d, "*.json"))):
     x = json.load(open(f))
+    if "roofline" not in x:  # reference-arm lines
+        continue
     h = x.get("halo") or {}
     print(f"{os.path.basename(f)[:-5]:18s} N={x['n_gpus']} {x['config']['mode']:8s} "
           f"{x['value']:8.1f} GPts/s  {x['ms_per_step']:7.3f} ms/step  frac {x['roofline']['frac']:.3f}  "
