@@ -370,7 +370,7 @@ static int launch_tti_stream(const Op& op, const Geom& g, const int64_t full[3],
 #define SDMP_GOP_TY 8
 #endif
 #ifndef SDMP_UOP_TY
-#define SDMP_UOP_TY 12
+#define SDMP_UOP_TY 11  // r04 A/B: 12 warps (168-register cap) beat 13 (128 cap): 67.4 vs 66.3 GPts/s
 #endif
     constexpr int VG = upd ? SDMP_UOP_VN : SDMP_GOP_V;
     if (ny <= 8) return launch_stream_op<R, 8, VG>(op, g, full, arrs, st, push);

@@ -10,3 +10,4 @@ $NCU --set full --clock-control none --import-source on --kernel-name-base deman
   -o $O/star_tma_so8_1024 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_full.log 2>&1
 $NCU -i $O/star_tma_so8_1024.ncu-rep --page raw --csv > $O/star_tma_so8_1024_raw.csv 2>&1
 timeout 2400 python -m pytest tests -m gpu -q --timeout 1500 > $O/pytest_gpu.txt 2>&1; echo "rc=$?" >> $O/pytest_gpu.txt
+bash tools/family_table.sh > $O/family.txt 2>&1; cp gpurun_out/family_table.jsonl $O/family_table.jsonl
