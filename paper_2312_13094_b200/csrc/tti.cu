@@ -396,7 +396,10 @@ static int launch_tti_stream(const Op& op, const Geom& g, const int64_t full[3],
 #define SDMP_TTI_UTY7_MINR 7
 #endif
     constexpr int TYU = R >= SDMP_TTI_UTY7_MINR ? 7 : SDMP_TTI_UTYW;
-    constexpr int TYW = upd ? TYU : (R <= 6 ? 16 : SDMP_TTI_GTYW);
+#ifndef SDMP_TTI_GTYM
+#define SDMP_TTI_GTYM 16
+#endif
+    constexpr int TYW = upd ? TYU : (R <= 6 ? SDMP_TTI_GTYM : SDMP_TTI_GTYW);
     constexpr int VW = upd ? SDMP_TTI_UVW : 2;
     constexpr int TYT = upd && R >= SDMP_TTI_UTY7_MINR ? 7 : 8;
     if (ny <= 8) return launch_stream_op<R, TYT, VW>(op, g, full, arrs, st, push);
