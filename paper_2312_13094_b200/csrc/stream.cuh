@@ -47,7 +47,8 @@ constexpr unsigned kHaloYZ = 0xFFFFFFFFu;
 __host__ __device__ constexpr bool halo_y(unsigned m, int c) { return (m >> (2 * c)) & 1u; }
 __host__ __device__ constexpr bool halo_z(unsigned m, int c) { return (m >> (2 * c + 1)) & 1u; }
 
-template <int R, int TY, int V, int NF, int NC, int NP, int CT = 1, unsigned M = kHaloYZ>
+template <int R, int TY, int V, int NF, int NC, int NP, int CT = 1, unsigned M = kHaloYZ,
+          int RB = 1>
 struct SLayout {
   static constexpr int TZ = kSZ * V;
   static constexpr int OFF = sround4(R);
@@ -71,7 +72,7 @@ struct SLayout {
   static constexpr int S0 = (220 * 1024) / CT / STAGE;  // CT resident CTAs per SM
   static constexpr int S = S0 > 4 ? 4 : (S0 < 2 ? 2 : S0);
   static constexpr int BYTES = S * STAGE + 2 * S * 8;
-  static constexpr int THREADS = 32 * (TY + 1);
+  static constexpr int THREADS = 32 * (TY / RB + 1);  // consumer warps + producer
   static constexpr uint32_t TX_FRONT = NF * FRONT;
   static constexpr uint32_t TX_MAIN = NF * FRONT + ctx_bytes() + NP * FRONT;
 };
@@ -85,6 +86,18 @@ struct TMaps {
 // bound for the large ops; pointwise operands loaded straight from global
 // memory one plane ahead instead of TMA-staged — latency bound, 1.3-1.6x
 // slower stress phases.)
+
+// Op::kRows (optional, default 1): y rows per consumer thread.  With 2 the
+// two rows' point() calls sit in one block, so the y taps they share (row
+// y+1's tap at dy is row y's at dy+1) are loaded from shared memory once.
+template <class Op, class = void>
+struct RowsOf {
+  static constexpr int value = 1;
+};
+template <class Op>
+struct RowsOf<Op, std::void_t<decltype(Op::kRows)>> {
+  static constexpr int value = Op::kRows;
+};
 
 // Op::kCtas (optional, default 1): resident CTAs per SM (launch bounds and
 // the shared-memory ring are sized for it)
@@ -101,7 +114,7 @@ struct CtasOf<Op, std::void_t<decltype(Op::kCtas)>> {
 // (at most 9 warps), so taller tiles keep their full register budget
 template <class Op, int TY>
 constexpr int ctas_for() {
-  return TY + 1 <= 9 ? CtasOf<Op>::value : 1;
+  return TY / RowsOf<Op>::value + 1 <= 9 ? CtasOf<Op>::value : 1;
 }
 
 // x-window unroll (stream_kernel): U = 2 planes per group where it was
@@ -234,13 +247,17 @@ __device__ __forceinline__ void vstore(float* p, int64_t idx, V2 v, bool m0, boo
 }
 
 template <int R, int TY, int V, class Op>
-__global__ void __launch_bounds__(SLayout<R, TY, V, Op::NF, Op::NC, Op::NP>::THREADS,
-                                  (ctas_for<Op, TY>()))
+__global__ void __launch_bounds__(
+    SLayout<R, TY, V, Op::NF, Op::NC, Op::NP, 1, kHaloYZ, RowsOf<Op>::value>::THREADS,
+    (ctas_for<Op, TY>()))
 stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, const int xchunk,
               const __grid_constant__ Push push) {
   constexpr int NF = Op::NF, NC = Op::NC, NP = Op::NP;
   constexpr unsigned M = CHaloOf<Op>::value;
-  using L = SLayout<R, TY, V, NF, NC, NP, ctas_for<Op, TY>(), M>;
+  constexpr int RB = RowsOf<Op>::value;
+  constexpr int NCW = TY / RB;  // consumer warps
+  static_assert(TY % RB == 0, "tile rows must be a multiple of the rows per thread");
+  using L = SLayout<R, TY, V, NF, NC, NP, ctas_for<Op, TY>(), M, RB>;
   using T = typename VType<V>::T;
   // __align__(1024) keeps TMA destinations aligned without integer pointer
   // arithmetic, so the consumers keep shared-space pointers (LDS)
@@ -252,7 +269,7 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
   if (lane == 0 && warp == 0) {
     for (int s = 0; s < L::S; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], TY);
+      mbar_init(&empty_bar[s], NCW);
     }
     fence_barrier_init();
   }
@@ -265,7 +282,7 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
   const int xb = min(xa + xchunk, g.hi[0]);
   const int nit = (xb - xa) + 2 * R;
 
-  if (warp == TY) {  // producer
+  if (warp == NCW) {  // producer
     if (lane == 0) {
       for (int i = 0; i < nit; ++i) {
         const int s = i % L::S;
@@ -293,21 +310,26 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
     return;
   }
 
-  const int z = z0 + V * lane, y = y0 + warp;
-  const bool yin = y < g.hi[1];
-  const bool m0 = yin && z >= g.lo[2] && z < g.hi[2];
-  const bool m1 = V > 1 && yin && z + 1 >= g.lo[2] && z + 1 < g.hi[2];
-  const bool active = m0 || m1;
+  const int z = z0 + V * lane;
+  bool m0[RB], m1[RB];
+#pragma unroll
+  for (int j = 0; j < RB; ++j) {
+    const bool yin = y0 + warp * RB + j < g.hi[1];
+    m0[j] = yin && z >= g.lo[2] && z < g.hi[2];
+    m1[j] = V > 1 && yin && z + 1 >= g.lo[2] && z + 1 < g.hi[2];
+  }
   constexpr int W = 2 * R + 1;
   // x-windows unrolled by U planes: slots are constants inside the unrolled
   // group and the 2R live planes move down once per group (2R / U register
   // moves per plane instead of 2R; unroll_for)
   constexpr int U = unroll_for<Op, R>();
-  T w[NF > 0 ? NF : 1][W + U - 1];
+  T w[RB][NF > 0 ? NF : 1][W + U - 1];
 #pragma unroll
-  for (int f = 0; f < NF; ++f)
+  for (int j = 0; j < RB; ++j)
 #pragma unroll
-    for (int k = 0; k < W + U - 1; ++k) w[f][k] = vconst<T>(0.f);
+    for (int f = 0; f < NF; ++f)
+#pragma unroll
+      for (int k = 0; k < W + U - 1; ++k) w[j][f][k] = vconst<T>(0.f);
 
   for (int i0 = 0; i0 < nit; i0 += U) {
 #pragma unroll
@@ -318,22 +340,32 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
         mbar_wait(&full_bar[s], (i / L::S) & 1);
         const unsigned char* st = sm + s * L::STAGE;
 #pragma unroll
-        for (int f = 0; f < NF; ++f)
-          w[f][2 * R + u] = vload<V>(reinterpret_cast<const float*>(st + f * L::FRONT) +
-                                     warp * L::TZ + V * lane);
-        if (i >= 2 * R && active) {
+        for (int j = 0; j < RB; ++j)
+#pragma unroll
+          for (int f = 0; f < NF; ++f)
+            w[j][f][2 * R + u] = vload<V>(reinterpret_cast<const float*>(st + f * L::FRONT) +
+                                          (warp * RB + j) * L::TZ + V * lane);
+        if (i >= 2 * R) {
           const int x = xa + i - 2 * R;
-          StreamCtx<R, TY, V, NF, NC, NP, U, M> ctx{w, st, warp, lane, u, &push, x, y, z};
-          op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0, m1);
+#pragma unroll
+          for (int j = 0; j < RB; ++j) {
+            const int row = warp * RB + j, y = y0 + row;
+            if (m0[j] || m1[j]) {
+              StreamCtx<R, TY, V, NF, NC, NP, U, M> ctx{w[j], st, row, lane, u, &push, x, y, z};
+              op.template point<R>(ctx, (int64_t)x * g.sx + (int64_t)y * g.sy + z, m0[j], m1[j]);
+            }
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);
       }
     }
 #pragma unroll
-    for (int f = 0; f < NF; ++f)
+    for (int j = 0; j < RB; ++j)
 #pragma unroll
-      for (int k = 0; k < 2 * R; ++k) w[f][k] = w[f][k + U];
+      for (int f = 0; f < NF; ++f)
+#pragma unroll
+        for (int k = 0; k < 2 * R; ++k) w[j][f][k] = w[j][f][k + U];
   }
 }
 
@@ -360,7 +392,8 @@ inline int stream_chunks(int64_t tiles, int nx, int R, int ctas = 1) {
 template <int R, int TY, int V, class Op>
 int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const float* const* ptrs,
                      cudaStream_t st, const Push* push = nullptr) {
-  using L = SLayout<R, TY, V, Op::NF, Op::NC, Op::NP, ctas_for<Op, TY>(), CHaloOf<Op>::value>;
+  using L = SLayout<R, TY, V, Op::NF, Op::NC, Op::NP, ctas_for<Op, TY>(), CHaloOf<Op>::value,
+                    RowsOf<Op>::value>;
   static_assert(Op::NF + Op::NC + Op::NP <= kMaxMaps, "too many tensor maps");
   static int attr_dev = -1;
   int dev = 0;
@@ -390,7 +423,7 @@ int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const f
   const int chunk = (nx + nch - 1) / nch;
   nch = (nx + chunk - 1) / chunk;
   SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");
-  dim3 grid(tz, ty, nch), block(32, TY + 1);
+  dim3 grid(tz, ty, nch), block(32, TY / RowsOf<Op>::value + 1);
   const bool dbg = getenv("SDMP_DEBUG") != nullptr;
   if (dbg)
     fprintf(stderr,

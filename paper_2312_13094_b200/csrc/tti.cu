@@ -242,9 +242,13 @@ struct GAcc {
 #ifndef SDMP_GOP_V
 #define SDMP_GOP_V 2
 #endif
+#ifndef SDMP_GOP_ROWS
+#define SDMP_GOP_ROWS 1
+#endif
 struct GOp {
   static constexpr int NF = 2, NC = 2, NP = 3;
   static constexpr int kCtas = SDMP_GOP_CTAS;
+  static constexpr int kRows = SDMP_GOP_ROWS;
   float* out[2];
   TTICoef k;
   template <int R, class Ctx>
