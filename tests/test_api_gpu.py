@@ -95,7 +95,7 @@ def test_modes_bitwise_equal_single_rank():
         assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
 
 
-@pytest.mark.parametrize("so", [4, 8, 12, 16])
+@pytest.mark.parametrize("so", [4, 6, 8, 12, 16])
 def test_tti_vs_oracle(so):
     shape, steps = (28, 24, 32), 10
     grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
@@ -172,8 +172,9 @@ def test_star_kernels_bitwise_equal_generic(so, monkeypatch):
     assert np.abs(outs[0][0]).max() > 0
 
 
-@pytest.mark.parametrize("family,so", [("tti", 4), ("tti", 8), ("tti", 12), ("tti", 16),
-                                       ("rotated", 4), ("rotated", 8), ("elastic", 8),
+@pytest.mark.parametrize("family,so", [("tti", 4), ("tti", 6), ("tti", 8), ("tti", 12),
+                                       ("tti", 16), ("rotated", 4), ("rotated", 6),
+                                       ("rotated", 8), ("rotated", 12), ("elastic", 8),
                                        ("elastic", 4), ("elastic", 16), ("visco", 16),
                                        ("visco", 8)])
 def test_stream_kernels_bitwise_equal_generic(family, so, monkeypatch):
@@ -306,7 +307,7 @@ def test_damped_acoustic_vs_oracle(so):
     assert np.any(coef["B"] > -0.999)
 
 
-@pytest.mark.parametrize("so", [4, 8, 12])
+@pytest.mark.parametrize("so", [4, 6, 8, 12])
 def test_rotated_gxx_vs_oracle(so):
     """The SPEC's tti_gxx_kernel (single-field rotated operator) through the
     public API vs the oracle on the same fp32 fields."""
