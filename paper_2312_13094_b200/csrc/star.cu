@@ -253,7 +253,12 @@ struct TmaCfg {
   static constexpr int FRONT = kTZ * TY * 4;
   static constexpr int CENTER = ((CZ * CY * 4) + 127) & ~127;
   static constexpr int STAGE = 3 * FRONT + CENTER;
-  static constexpr int S = 4;
+#ifndef SDMP_STAR_STAGES
+#define SDMP_STAR_STAGES 4
+#endif
+  // pipeline depth: SDMP_STAR_STAGES planes in flight, fewer if they do not fit
+  static constexpr int S0 = (224 * 1024 - 2048) / STAGE;
+  static constexpr int S = SDMP_STAR_STAGES < S0 ? SDMP_STAR_STAGES : S0;
   static constexpr int BYTES = S * STAGE + 2 * S * 8 + 128;
   static constexpr int THREADS = 32 * (TY + 1);
 };
