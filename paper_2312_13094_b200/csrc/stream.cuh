@@ -70,7 +70,10 @@ struct SLayout {
   static constexpr int CENTERS = coff(NC);
   static constexpr int STAGE = NF * FRONT + CENTERS + NP * FRONT;
   static constexpr int S0 = (220 * 1024) / CT / STAGE;  // CT resident CTAs per SM
-  static constexpr int S = S0 > 4 ? 4 : (S0 < 2 ? 2 : S0);
+#ifndef SDMP_STREAM_STAGES
+#define SDMP_STREAM_STAGES 4
+#endif
+  static constexpr int S = S0 > SDMP_STREAM_STAGES ? SDMP_STREAM_STAGES : (S0 < 2 ? 2 : S0);
   static constexpr int BYTES = S * STAGE + 2 * S * 8;
   static constexpr int THREADS = 32 * (TY / RB + 1);  // consumer warps + producer
   static constexpr uint32_t TX_FRONT = NF * FRONT;
