@@ -153,7 +153,9 @@ int sdmp_pack(void* stream, const float* field, const int64_t full[3], const int
 int sdmp_unpack(void* stream, float* field, const int64_t full[3], const int64_t lo[3],
                 const int64_t hi[3], const float* buf);
 /* Box copy between two FULL arrays (either may be a peer/IPC pointer).
- * engine 0: copy engine (cudaMemcpy3DAsync); 1: SM kernel (peer stores). */
+ * engine 0: copy engine (cudaMemcpy3DAsync); 1: SM kernel (peer stores);
+ * 2: the batched post kernel of diagonal / basic mode, one box (16-byte
+ * peer stores, one warp per z row). */
 int sdmp_copy_box(void* stream, const float* src, const int64_t src_full[3],
                   const int64_t src_lo[3], float* dst, const int64_t dst_full[3],
                   const int64_t dst_lo[3], const int64_t extent[3], int32_t engine);

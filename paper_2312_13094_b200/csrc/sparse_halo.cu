@@ -199,6 +199,20 @@ int copy_box(cudaStream_t st, const float* src, const int64_t sfull[3], const in
     SDMP_CHECK(dlo[a] >= 0 && dlo[a] + ext[a] <= dfull[a], "destination box outside array");
   }
   if (ext[0] == 0 || ext[1] == 0 || ext[2] == 0) return SDMP_OK;
+  if (engine == 2) {  // the batched post kernel (k_multi_copy) with one box
+    MultiCopy mc;
+    CopyMsg& c = mc.m[0];
+    c.src = src; c.dst = dst;
+    c.ssy = sfull[2]; c.ssx = sfull[1] * sfull[2];
+    c.dsy = dfull[2]; c.dsx = dfull[1] * dfull[2];
+    c.soff = slo[0] * c.ssx + slo[1] * c.ssy + slo[2];
+    c.doff = dlo[0] * c.dsx + dlo[1] * c.dsy + dlo[2];
+    c.ex = (int)ext[0]; c.ey = (int)ext[1]; c.ez = (int)ext[2];
+    mc.n = 1;
+    mc.row0[0] = 0;
+    mc.rows = (int64_t)c.ex * c.ey;
+    return multi_copy(st, mc);
+  }
   if (engine == 0) {
     cudaMemcpy3DParms p = {};
     p.srcPtr = make_cudaPitchedPtr((void*)src, sfull[2] * sizeof(float), sfull[2], sfull[1]);

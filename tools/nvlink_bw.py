@@ -5,8 +5,10 @@ timed with CUDA events on the issuing stream of GPU 0:
   diagonal / basic mode, for the BASELINE message shapes: an x-face (R
   planes) and a y-face (R rows) of a 1024^3 rank with halo 8, with and
   without whole-z rows (SDMP_WHOLE_Z);
-* SM stores into peer memory (`sdmp_copy_box` engine 1: the same store path
-  the fused full-mode kernels use for their halo push), same shapes;
+* SM stores into peer memory (`sdmp_copy_box` engine 1, scalar stores; engine
+  2, the batched post kernel with 16-byte stores -- the store path of the
+  diagonal / basic default and, per point, of the fused full-mode push),
+  same shapes;
 * a plain 1 GiB contiguous peer copy as the link ceiling.
 
 Prints one JSON line per case: bytes moved, ms, GB/s, fraction of 900 GB/s.
@@ -66,11 +68,13 @@ def main():
             if whole_z:
                 s_lo[2], d_lo[2], e[2] = 0, 0, full[2]
             nbytes = 4 * e[0] * e[1] * e[2]
-            for engine in (0, 1):
+            for engine in (0, 1, 2):
                 ms = timed(lambda: R.copy_box(src, full, s_lo, dst, full, d_lo, e, engine), a.reps)
                 out.append({"case": name, "whole_z": whole_z,
-                            "engine": "copy engine (cudaMemcpy3DAsync)" if engine == 0
-                            else "SM peer stores", "bytes": nbytes, "ms": ms,
+                            "engine": ["copy engine (cudaMemcpy3DAsync)",
+                                       "SM peer stores (one kernel per box)",
+                                       "SM peer stores (batched post kernel, 16-byte)"][engine],
+                            "bytes": nbytes, "ms": ms,
                             "gbs": nbytes / (ms * 1e-3) / 1e9,
                             "frac_of_900": nbytes / (ms * 1e-3) / 1e9 / 900.0})
     big_s = torch.empty(1 << 28, device="cuda:0")
