@@ -258,6 +258,7 @@ struct VelAcc {
 template <bool COL = false>
 struct VelOpT {
   static constexpr int NF = 3, NC = 5, NP = 4;
+  static constexpr int kStagesWide = 6;  // r04 A/B (stream.cuh StagesWideOf)
   static constexpr int kCtas = SDMP_VEL_CTAS;
   // centre tiles tapped along one axis stage only that halo: tyy, txy (y),
   // tzz, txz (z); tyz both (r04: -18% / -35% staged bytes at SO-8 / SO-16)
@@ -319,6 +320,7 @@ struct StressOpT {
 #endif
 struct ViscoOp {
   static constexpr int NF = 3, NC = 3, NP = 15;
+  static constexpr int kStagesWide = 6;  // r04 A/B (stream.cuh StagesWideOf)
   static constexpr int kCtas = SDMP_VISCO_CTAS;
   static constexpr int kUnrollMinR = 5;  // unroll_for: U = 1 below SO-10 (r03 A/B)
   float* out[12];

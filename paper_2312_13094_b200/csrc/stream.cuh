@@ -43,12 +43,15 @@ __host__ __device__ constexpr int sround4(int r) { return (r + 3) & ~3; }
 // the R-row y halo, bit 2c+1: the OFF-column z halo).  An op whose tile is
 // only tapped along one axis stages just that halo (Op::kCHalo; default all
 // tiles carry both).
+#ifndef SDMP_STREAM_STAGES
+#define SDMP_STREAM_STAGES 4
+#endif
 constexpr unsigned kHaloYZ = 0xFFFFFFFFu;
 __host__ __device__ constexpr bool halo_y(unsigned m, int c) { return (m >> (2 * c)) & 1u; }
 __host__ __device__ constexpr bool halo_z(unsigned m, int c) { return (m >> (2 * c + 1)) & 1u; }
 
 template <int R, int TY, int V, int NF, int NC, int NP, int CT = 1, unsigned M = kHaloYZ,
-          int RB = 1>
+          int RB = 1, int SMAX = SDMP_STREAM_STAGES>
 struct SLayout {
   static constexpr int TZ = kSZ * V;
   static constexpr int OFF = sround4(R);
@@ -70,10 +73,7 @@ struct SLayout {
   static constexpr int CENTERS = coff(NC);
   static constexpr int STAGE = NF * FRONT + CENTERS + NP * FRONT;
   static constexpr int S0 = (220 * 1024) / CT / STAGE;  // CT resident CTAs per SM
-#ifndef SDMP_STREAM_STAGES
-#define SDMP_STREAM_STAGES 4
-#endif
-  static constexpr int S = S0 > SDMP_STREAM_STAGES ? SDMP_STREAM_STAGES : (S0 < 2 ? 2 : S0);
+  static constexpr int S = S0 > SMAX ? SMAX : (S0 < 2 ? 2 : S0);
   static constexpr int BYTES = S * STAGE + 2 * S * 8;
   static constexpr int THREADS = 32 * (TY / RB + 1);  // consumer warps + producer
   static constexpr uint32_t TX_FRONT = NF * FRONT;
@@ -138,6 +138,22 @@ struct UnrollMinR<Op, std::void_t<decltype(Op::kUnrollMinR)>> {
 template <class Op, int R>
 constexpr int unroll_for() {
   return SDMP_STREAM_UNROLL ? SDMP_STREAM_UNROLL : (R >= UnrollMinR<Op>::value ? 2 : 1);
+}
+
+// Op::kStagesWide (optional): pipeline depth cap for R >= 5 (default 4).
+// r04 A/B: 6 stages help the wide visco stress (+4-5%), rotated (+7%) and
+// staggered velocity (+2%) ops and cost the others (damped SO-16 -12%).
+template <class Op, class = void>
+struct StagesWideOf {
+  static constexpr int value = SDMP_STREAM_STAGES;
+};
+template <class Op>
+struct StagesWideOf<Op, std::void_t<decltype(Op::kStagesWide)>> {
+  static constexpr int value = Op::kStagesWide;
+};
+template <class Op, int R>
+constexpr int stages_for() {
+  return R >= 5 ? StagesWideOf<Op>::value : SDMP_STREAM_STAGES;
 }
 
 template <class Op, class = void>
@@ -260,7 +276,7 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
   constexpr int RB = RowsOf<Op>::value;
   constexpr int NCW = TY / RB;  // consumer warps
   static_assert(TY % RB == 0, "tile rows must be a multiple of the rows per thread");
-  using L = SLayout<R, TY, V, NF, NC, NP, ctas_for<Op, TY>(), M, RB>;
+  using L = SLayout<R, TY, V, NF, NC, NP, ctas_for<Op, TY>(), M, RB, stages_for<Op, R>()>;
   using T = typename VType<V>::T;
   // __align__(1024) keeps TMA destinations aligned without integer pointer
   // arithmetic, so the consumers keep shared-space pointers (LDS)
@@ -396,7 +412,7 @@ template <int R, int TY, int V, class Op>
 int launch_stream_op(const Op& op, const Geom& g, const int64_t full[3], const float* const* ptrs,
                      cudaStream_t st, const Push* push = nullptr) {
   using L = SLayout<R, TY, V, Op::NF, Op::NC, Op::NP, ctas_for<Op, TY>(), CHaloOf<Op>::value,
-                    RowsOf<Op>::value>;
+                    RowsOf<Op>::value, stages_for<Op, R>()>;
   static_assert(Op::NF + Op::NC + Op::NP <= kMaxMaps, "too many tensor maps");
   static int attr_dev = -1;
   int dev = 0;

@@ -318,6 +318,7 @@ struct RGAcc {
 
 struct RGOp {
   static constexpr int NF = 1, NC = 1, NP = 3;
+  static constexpr int kStagesWide = 6;  // r04 A/B (stream.cuh StagesWideOf)
   float* out;
   TTICoef k;
   template <int R, class Ctx>
@@ -344,6 +345,7 @@ struct RUAcc {
 
 struct RUOp {
   static constexpr int NF = 2, NC = 3, NP = 3;
+  static constexpr int kStagesWide = 6;  // r04 A/B (stream.cuh StagesWideOf)
   static constexpr unsigned kCHalo = 1u | (2u << 2) | (3u << 4);  // a_y: y, a_z: z, g: both
   float* out;
   TTICoef k;
