@@ -2,7 +2,7 @@
 timed with CUDA events on the launching stream (development tool; the
 contract benchmark is bench.py).
 
-    python tools/kbench.py --kernel star --n 1024 --so 8 --variant 2
+    python tools/kbench.py --kernel star --n 1024 --so 8 --variant 3
 """
 import argparse
 import json
