@@ -125,9 +125,6 @@ static int box_copy_kernel(cudaStream_t st, const BoxXfer& b) {
 // loads / peer stores when the row is 16-byte aligned on both sides (the
 // whole-z rows of the product always are), scalar otherwise.
 
-#ifndef SDMP_COPY_V8
-#define SDMP_COPY_V8 1
-#endif
 __global__ void __launch_bounds__(256) k_multi_copy(const __grid_constant__ MultiCopy mc) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -141,26 +138,7 @@ __global__ void __launch_bounds__(256) k_multi_copy(const __grid_constant__ Mult
     const float* s = c.src + c.soff + x * c.ssx + y * c.ssy;
     float* d = c.dst + c.doff + x * c.dsx + y * c.dsy;
     const int ez = c.ez;
-    const uintptr_t al = reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d);
-#if SDMP_COPY_V8
-    if ((al & 31) == 0) {  // 32-byte loads / peer stores (LDG/STG.256, sm_100)
-      const int n8 = ez >> 3;
-      for (int i = lane; i < n8; i += 32) {
-        float v[8];
-        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
-                       "=f"(v[6]), "=f"(v[7])
-                     : "l"(s + 8 * i));
-        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(d + 8 * i),
-                     "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]),
-                     "f"(v[7])
-                     : "memory");
-      }
-      for (int i = (n8 << 3) + lane; i < ez; i += 32) d[i] = s[i];
-      continue;
-    }
-#endif
-    if ((al & 15) == 0) {
+    if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0) {
       const int n4 = ez >> 2;
       const float4* s4 = reinterpret_cast<const float4*>(s);
       float4* d4 = reinterpret_cast<float4*>(d);
