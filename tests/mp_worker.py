@@ -163,7 +163,22 @@ def main():
              ("visco", elastic, {"visco": True, "so": 16})]
     only = os.environ.get("FAMILIES")
     if only:
-        cases = [c for c in cases if c[0] in only.split(",")]
+        # "<family><SO>" (e.g. acoustic2, elastic_col4) runs a family at
+        # another space order (the SPEC.md:702 matrix over SDO {2, 4, 8})
+        import re
+        base = {c[0]: c for c in cases}
+        picked = []
+        for name in only.split(","):
+            if name in base:
+                picked.append(base[name])
+                continue
+            mt = re.fullmatch(r"([a-z_]+?)(\d+)", name)
+            if mt and mt.group(1) in base:
+                fam, build, kw = base[mt.group(1)]
+                picked.append((name, build, dict(kw, so=int(mt.group(2)))))
+            else:
+                raise SystemExit(f"unknown family {name!r}")
+        cases = picked
     for fam, build, kw in cases:
         for mode in ("basic", "diagonal", "full"):
             ext = tuple(10.0 * (n - 1) for n in shape)

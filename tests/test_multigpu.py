@@ -106,6 +106,17 @@ def test_eight_ranks_4x2_layout():
 
 
 @needs_gpu
+def test_spec_acceptance_matrix_space_orders():
+    """kernel x SDO {2, 4, 8} x mode -- the SPEC's four kernels
+    (diffusion, acoustic, collocated elastic, tti_gxx = rotated) at the space
+    orders the other tests do not already run, on 4 ranks (2,2,1)."""
+    fams = ("diffusion2,diffusion8,acoustic2,acoustic4,elastic_col2,elastic_col4,"
+            "rotated2")
+    rc, rep, err = _run(4, "2,2,1", "44,40,32", fams, steps=8, port=29527)
+    _check(rc, rep, err, fams)
+
+
+@needs_gpu
 @pytest.mark.parametrize("engine", ["sm", "ce"])
 def test_halo_copy_engines(engine):
     """The alternatives to the default batched SM posts (SDMP_COPY_ENGINE=sm:
