@@ -265,3 +265,69 @@ def test_rot_update_entry_point():
                  (lo, hi), want)
     s = tuple(slice(x, y) for x, y in zip(lo, hi))
     assert rel_l2(u1.cpu().numpy()[s], want[s]) <= REL
+
+
+@pytest.mark.parametrize("so", [4, 8])
+def test_tti_and_rot_bound_scale_flag(so):
+    """radius | SDMP_VARIANT_M_IS_SCALE: the m operand holds the bound
+    RN(dt2 / m) (what the plan passes) -- bit-identical to dividing per
+    point, for the single-pass (SO-4 TTI, both rotated) and two-pass (SO-8
+    TTI) kernels."""
+    r = so // 2
+    full = (16 + 4 * so, 16 + 4 * so, 24 + 4 * so)
+    lo, hi = (2 * so,) * 3, tuple(n - 2 * so for n in full)
+    rng = np.random.default_rng(so + 7)
+    p0, p2, r0, r2 = (np.float32(rng.standard_normal(full)) for _ in range(4))
+    m = np.float32(0.2 + 0.2 * rng.random(full))
+    epsp = np.float32(1.0 + 0.3 * rng.random(full))
+    delp = np.float32(1.0 + 0.1 * rng.random(full))
+    th, ph = rng.random(full) * 0.6, rng.random(full) * 0.6
+    a = [np.float32(np.sin(th) * np.cos(ph)), np.float32(np.sin(th) * np.sin(ph)),
+         np.float32(np.cos(th))]
+    w2 = [float(c) for c in S.fd_coefficients(2, so)]
+    w1 = [float(c) for c in S.fd_coefficients(1, so)]
+    lap = R.coeff_table([np.float32([w2[r + k] / 100.0 for k in range(r + 1)])] * 3, NC)
+    d1 = R.coeff_table([np.float32([0.0] + [w1[r + k] / 10.0 for k in range(1, r + 1)])] * 3, NC)
+    dt2 = np.float32(0.25)
+    scale = np.float32(dt2 / m)   # IEEE round-to-nearest fp32 division
+    fp = lambda t: t.ctypes.data_as(C.POINTER(C.c_float))  # noqa: E731
+    outs = []
+    for mm, rad in ((m, r), (scale, r | R.VARIANT_M_IS_SCALE)):
+        ins = [dev(x) for x in (p0, p2, r0, r2, mm, epsp, delp, *a)]
+        p1, r1 = torch.zeros_like(ins[0]), torch.zeros_like(ins[0])
+        call("sdmp_tti_update", None, ptrs(ins), C.c_void_p(p1.data_ptr()),
+             C.c_void_p(r1.data_ptr()), arr(C.c_int64, full), arr(C.c_int64, lo),
+             arr(C.c_int64, hi), rad, fp(lap), fp(d1), C.c_float(float(dt2)), 0)
+        rins = [dev(x) for x in (p0, p2, mm, *a)]
+        u1 = torch.zeros_like(rins[0])
+        call("sdmp_rot_update", None, ptrs(rins), C.c_void_p(u1.data_ptr()),
+             arr(C.c_int64, full), arr(C.c_int64, lo), arr(C.c_int64, hi), rad, fp(d1),
+             C.c_float(float(dt2)))
+        outs.append([t.cpu().numpy() for t in (p1, r1, u1)])
+    for x, y in zip(*outs):
+        assert np.array_equal(x, y)
+        assert np.abs(x).max() > 0
+
+
+def test_copy_box_engines_identical():
+    """sdmp_copy_box engine 0 (copy engine), 1 (SM, one kernel per box) and 2
+    (the batched post kernel) move the same box bit for bit, including
+    rows that are not 16-byte aligned (scalar path)."""
+    full = (20, 18, 40)
+    rng = np.random.default_rng(3)
+    src = dev(rng.standard_normal(full))
+    for slo, dlo, ext in (((2, 3, 8), (1, 0, 8), (4, 5, 24)), ((2, 3, 1), (1, 0, 3), (4, 5, 30)),
+                          ((0, 0, 0), (0, 0, 0), (20, 18, 40))):
+        res = []
+        for engine in (0, 1, 2):
+            dst = torch.zeros_like(src)
+            call("sdmp_copy_box", None, C.c_void_p(src.data_ptr()), arr(C.c_int64, full),
+                 arr(C.c_int64, slo), C.c_void_p(dst.data_ptr()), arr(C.c_int64, full),
+                 arr(C.c_int64, dlo), arr(C.c_int64, ext), engine)
+            res.append(dst.cpu().numpy())
+        want = np.zeros(full, np.float32)
+        sv = src.cpu().numpy()
+        want[tuple(slice(d, d + e) for d, e in zip(dlo, ext))] = \
+            sv[tuple(slice(s_, s_ + e) for s_, e in zip(slo, ext))]
+        for r_ in res:
+            assert np.array_equal(r_, want)
