@@ -119,6 +119,11 @@ inline bool box_empty(const Geom& g) {
   return g.hi[0] <= g.lo[0] || g.hi[1] <= g.lo[1] || g.hi[2] <= g.lo[2];
 }
 
+// CTA-partial barrier (bar.sync id, nthreads) for warp-specialised kernels
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 inline int num_sms() {
   static int n = 0;
   if (n == 0) {

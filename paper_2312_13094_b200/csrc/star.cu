@@ -14,17 +14,19 @@
 //
 //  * star_generic: one thread per point, taps through L1/L2.  Any radius,
 //    any alignment, 2D (radius_z = 0) included.  Used for thin OWNED slabs.
-//  * star_tma<R,TY> / star_tma2<R,TY>: HBM-roofline kernels.  A CTA owns a
+//  * star_tma<R,TY> / star_tma2<R,TY> / star_tmem<R,TY>: HBM-roofline kernels.  A CTA owns a
 //    128(z) x TY(y) tile and streams along x (slowest axis); a producer warp
 //    stages plane tiles with TMA, each consumer thread keeps a float4
 //    x-window of 2R+1 planes in registers and reads y/z taps from the staged
-//    centre plane.  u0 is read from DRAM once (halo re-reads of neighbouring
+//    centre plane (star_tmem: the x-window lives in tensor memory instead).
+//    u0 is read from DRAM once (halo re-reads of neighbouring
 //    tiles hit L2), u2 and m streamed once, u1 written once: 16 B / point.
 #include <cstdlib>
 
 #include "common.cuh"
 #include "stream.cuh"
 #include "tma.cuh"
+#include "tmem.cuh"
 #include "vmath.cuh"
 
 namespace sdmp {
@@ -657,6 +659,241 @@ static int launch_tma2(const StarParams& p, cudaStream_t st, const int64_t full[
 }
 
 // ---------------------------------------------------------------------------
+// Widest stencils: star_tma2's pipeline with the x-window in TENSOR MEMORY.
+// At R = 8 the two 17-plane register windows (144 registers) pin star_tma2
+// to 8 warps per SM, where it is latency bound (profiles/r03_unroll.md).
+// Here the window is a ring of 2R plane slots in TMEM: each consumer thread
+// owns 8 columns per slot (its 2 rows x 4 z points) of its warp's lane
+// quarter.  Per plane a thread reads the 2R - 1 older planes back with
+// tcgen05.ld (64 B / point, ~a quarter of TMEM read bandwidth at the HBM
+// roofline), takes the centre plane from the staged centre tile and the
+// newest plane from the front tile, and writes the newest plane into the
+// slot the oldest one just vacated.  Registers drop to ~100, so TY / 2 = 12
+// consumer warps run per SM.  Arithmetic is star_tma2's, term for term.
+#ifndef SDMP_TMEM_KC
+#define SDMP_TMEM_KC 4  // x-tap pairs per tcgen05.ld batch
+#endif
+#ifndef SDMP_TMEM_ROWS
+#define SDMP_TMEM_ROWS 24
+#endif
+template <int R, int TY>
+struct TmemCfg {
+  static constexpr int NW = TY / 2;                 // consumer warps
+  static constexpr int SLICES = (NW + 3) / 4;       // warps sharing a lane quarter
+  static constexpr int SLOT = 8;                    // columns per plane slot
+  static constexpr int COLS_USED = SLICES * 2 * R * SLOT;
+  static constexpr int COLS = COLS_USED <= 128 ? 128 : COLS_USED <= 256 ? 256 : 512;
+  static_assert(COLS_USED <= 512, "x-window ring does not fit TMEM");
+};
+
+template <int R, int TY>
+__global__ void __launch_bounds__(32 * (TY / 2 + 1), 1)
+star_tmem(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ CUtensorMap tm_center,
+          const __grid_constant__ CUtensorMap tm_u2, const __grid_constant__ CUtensorMap tm_m,
+          StarParams p, int xchunk, const Push push) {
+  using T = TmaCfg<R, TY>;
+  using M = TmemCfg<R, TY>;
+  constexpr int NW = M::NW;
+  constexpr int KC = SDMP_TMEM_KC;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = smraw;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sm + T::S * T::STAGE);
+  uint64_t* empty_bar = full_bar + T::S;
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(empty_bar + T::S);
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const bool has_u2 = p.u2 != nullptr, has_m = p.m != nullptr;
+  if (lane == 0 && warp == 0) {
+    for (int s = 0; s < T::S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], NW);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<M::COLS>(tbase);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const int z0 = p.g.lo[2] + blockIdx.x * kTZ;
+  const int y0 = p.g.lo[1] + blockIdx.y * TY;
+  const int xa = p.g.lo[0] + blockIdx.z * xchunk;
+  const int xb = min(xa + xchunk, p.g.hi[0]);
+  const int nit = (xb - xa) + 2 * R;
+
+  if (warp == NW) {  // producer
+    if (lane == 0) {
+      prefetch_tmap(&tm_front);
+      prefetch_tmap(&tm_center);
+      const uint32_t main_bytes =
+          T::FRONT + T::CZ * T::CY * 4 + (has_u2 ? T::FRONT : 0) + (has_m ? T::FRONT : 0);
+      for (int i = 0; i < nit; ++i) {
+        const int s = i % T::S;
+        mbar_wait(&empty_bar[s], ((i / T::S) & 1) ^ 1);
+        unsigned char* st = sm + s * T::STAGE;
+        const bool main = i >= 2 * R;
+        mbar_arrive_expect_tx(&full_bar[s], main ? main_bytes : (uint32_t)T::FRONT);
+        tma_load_3d(st, &tm_front, &full_bar[s], z0, y0, xa - R + i);
+        if (main) {
+          const int x = xa + i - 2 * R;
+          tma_load_3d(st + T::FRONT, &tm_center, &full_bar[s], z0 - T::OFF, y0 - R, x);
+          if (has_u2) tma_load_3d(st + T::FRONT + T::CENTER, &tm_u2, &full_bar[s], z0, y0, x);
+          if (has_m)
+            tma_load_3d(st + 2 * T::FRONT + T::CENTER, &tm_m, &full_bar[s], z0, y0, x);
+        }
+      }
+    }
+    return;
+  }
+
+  const int z = z0 + 4 * lane, r0 = 2 * warp;  // rows r0, r0 + 1 of the tile
+  const bool zin = z < p.g.hi[2];
+  const bool act0 = zin && (y0 + r0 < p.g.hi[1]), act1 = zin && (y0 + r0 + 1 < p.g.hi[1]);
+  const bool ract = y0 + r0 < p.g.hi[1];  // warp-uniform
+  // this warp's ring: lane quarter warp % 4, column slice warp / 4
+  const uint32_t ring = *tbase + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                        static_cast<uint32_t>((warp >> 2) * 2 * R * M::SLOT);
+  auto slot_addr = [&](int s) { return ring + static_cast<uint32_t>(s * M::SLOT); };
+
+  for (int i = 0; i < nit; ++i) {
+    const int s = i % T::S;
+    mbar_wait(&full_bar[s], (i / T::S) & 1);
+    const unsigned char* st = sm + s * T::STAGE;
+    if (ract) {
+      tmem_wait_st();  // last plane's slot write has landed (and freed its registers)
+      const float* front = reinterpret_cast<const float*>(st) + 4 * lane;
+      const float4 fa = *reinterpret_cast<const float4*>(front + r0 * kTZ);
+      const float4 fb = *reinterpret_cast<const float4*>(front + (r0 + 1) * kTZ);
+      const int snew = i % (2 * R);  // slot of this iteration's newest plane
+      if (i >= 2 * R) {
+        const int x = xa + i - 2 * R;
+        const float* crow = reinterpret_cast<const float*>(st + T::FRONT) + (r0 + R) * T::CZ +
+                            T::OFF + 4 * lane;
+        auto rowv = [&](int d) { return *reinterpret_cast<const float4*>(crow + d * T::CZ); };
+        const float4 c0a = rowv(0), c0b = rowv(1);
+        V2 l0[2], l1[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          l0[h] = vcmul(p.csum0, f4pair(c0a, h));
+          l1[h] = vcmul(p.csum0, f4pair(c0b, h));
+        }
+        // x taps: planes x -/+ k live in slots (scen -/+ k) mod 2R, scen =
+        // the centre plane's slot; x + R (slot scen + R = snew) is the front
+        const int scen = (i - R) % (2 * R);
+#pragma unroll
+        for (int k0 = 1; k0 <= R; k0 += KC) {
+          float4 ma[KC], mb[KC], pa[KC], pb[KC];
+#pragma unroll
+          for (int j = 0; j < KC; ++j) {
+            const int k = k0 + j;
+            if (k > R) break;
+            int sm_ = scen - k;
+            sm_ += sm_ < 0 ? 2 * R : 0;
+            tmem_ld8(slot_addr(sm_), ma[j], mb[j]);
+            if (k < R) {
+              int sp = scen + k;
+              sp -= sp >= 2 * R ? 2 * R : 0;
+              tmem_ld8(slot_addr(sp), pa[j], pb[j]);
+            }
+          }
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < KC; ++j) {
+            const int k = k0 + j;
+            if (k > R) break;
+            tmem_pin(ma[j]);
+            tmem_pin(mb[j]);
+            if (k < R) {
+              tmem_pin(pa[j]);
+              tmem_pin(pb[j]);
+            } else {
+              pa[j] = fa;
+              pb[j] = fb;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              l0[h] = vcfma(p.c[0][k], vadd(f4pair(ma[j], h), f4pair(pa[j], h)), l0[h]);
+              l1[h] = vcfma(p.c[0][k], vadd(f4pair(mb[j], h), f4pair(pb[j], h)), l1[h]);
+            }
+          }
+        }
+        // the oldest plane (x - R) has been read: its slot takes the newest
+        tmem_st8(slot_addr(snew), fa, fb);
+        // y taps (star_tma2's software-pipelined pairs)
+        float4 am = c0a, bk = c0b, bn;
+#pragma unroll
+        for (int k = 1; k <= R; ++k) {
+          const float4 ak = rowv(-k);
+          bn = rowv(k + 1);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            l0[h] = vcfma(p.c[1][k], vadd(f4pair(ak, h), f4pair(bk, h)), l0[h]);
+            l1[h] = vcfma(p.c[1][k], vadd(f4pair(am, h), f4pair(bn, h)), l1[h]);
+          }
+          am = ak;
+          bk = bn;
+        }
+        constexpr int NZW = (4 + 2 * T::OFF) / 4;
+        float zw[4 * NZW];
+        float out[4];
+        const float* pts = reinterpret_cast<const float*>(st + T::FRONT + T::CENTER) + 4 * lane;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          star_zwin<T::OFF>(zw, j == 0 ? c0a : c0b, crow + j * T::CZ, lane);
+          V2* l = j == 0 ? l0 : l1;
+          star_ztaps<R, T::OFF>(p, zw, l);
+          const int rr = r0 + j;
+          const float4 u2v = has_u2 ? *reinterpret_cast<const float4*>(pts + rr * kTZ)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 mv = has_m ? *reinterpret_cast<const float4*>(pts + T::FRONT / 4 + rr * kTZ)
+                                  : make_float4(1.f, 1.f, 1.f, 1.f);
+          star_finish4(p, l, j == 0 ? c0a : c0b, u2v, mv, out);
+          if (j == 0 ? act0 : act1) star_store4(p, push, x, y0 + rr, z, out);
+        }
+      } else {
+        tmem_st8(slot_addr(snew), fa, fb);  // filling the ring
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
+  }
+  tmem_wait_st();
+  tmem_fence_before();
+  named_sync(1, NW * 32);
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc<M::COLS>(*tbase);
+}
+
+template <int R, int TY>
+static int launch_tmem(const StarParams& p, cudaStream_t st, const int64_t full[3],
+                       const Push& push) {
+  using T = TmaCfg<R, TY>;
+  constexpr int BYTES = T::BYTES + 16;  // + the TMEM base address
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    SDMP_CUDA(cudaFuncSetAttribute(star_tmem<R, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   BYTES));
+    attr_dev = dev;
+  }
+  CUtensorMap tf, tc, t2, tm;
+  int rc = make_tmap_3d(&tf, p.u0, full, kTZ, TY, false);
+  if (!rc) rc = make_tmap_3d(&tc, p.u0, full, T::CZ, T::CY, false);
+  if (!rc) rc = make_tmap_3d(&t2, p.u2 ? p.u2 : p.u0, full, kTZ, TY, true);
+  if (!rc) rc = make_tmap_3d(&tm, p.m ? p.m : p.u0, full, kTZ, TY, true);
+  if (rc) return rc;
+  const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
+  const int tz = (nz + kTZ - 1) / kTZ, ty = (ny + TY - 1) / TY;
+  int nch = pick_chunks((int64_t)tz * ty, nx, R, 1);
+  const int chunk = (nx + nch - 1) / nch;
+  nch = (nx + chunk - 1) / chunk;
+  SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");
+  dim3 grid(tz, ty, nch), block(32, TY / 2 + 1);
+  star_tmem<R, TY><<<grid, block, BYTES, st>>>(tf, tc, t2, tm, p, chunk, push);
+  SDMP_LAUNCHED();
+  return SDMP_OK;
+}
+
+// ---------------------------------------------------------------------------
 // variable-coefficient star on the generic TMA stream engine: fronts {u0},
 // centre {u0}, points {u2 (if B), A, B (if present), S}; same per-point order
 // as star_point + star_finish
@@ -738,7 +975,8 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
   p.u0 = u0; p.u2 = (B == 0.0f) ? nullptr : u2; p.m = m; p.u1 = u1;
   p.m_is_scale = (variant & SDMP_VARIANT_M_IS_SCALE) ? 1 : 0;
   variant &= 0xff;
-  if (variant == 0) {  // SDMP_STAR_VARIANT (tests): 1 generic, 3 one-row TMA at every R
+  if (variant == 0) {  // SDMP_STAR_VARIANT (tests): 1 generic, 3 one-row TMA at every R,
+                       // 4 register-window two-row TMA at R >= 6
     const char* e = getenv("SDMP_STAR_VARIANT");
     variant = e ? atoi(e) : 0;
   }
@@ -759,10 +997,23 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
                           (((uintptr_t)u0 | (uintptr_t)u1 | (uintptr_t)u2 | (uintptr_t)m) % 16 == 0);
   // unaligned / unequal-radius boxes always take the generic kernel
   if (variant == 1 || !streamable) return launch_generic(p, st, push);
-  // wide stencils: two rows per thread.  16-row tiles (9 warps: ptxas caps
-  // registers at 168) while the two x-windows fit; R = 8 needs ~210
-  // registers, so 14-row tiles (8 warps, 255 registers)
-  if (variant == 0) {
+  // wide stencils: two rows per thread.  R >= 7: x-window in tensor memory
+  // (star_tmem, 24-row tiles, 12 consumer warps at 104 registers): SO-16
+  // 0.716 -> 0.846 and SO-14 0.794 -> 0.884 of the HBM roofline, SO-12 keeps
+  // the register window (0.936 vs 0.917; profiles/round2_ab_tmem.txt).
+  // star_tma2: 16-row tiles (9 warps: ptxas caps registers at 168) while the
+  // two x-windows fit; R = 8 needs ~210 registers, so 14-row tiles (8 warps)
+#ifndef SDMP_STAR_TMEM_MINR
+#define SDMP_STAR_TMEM_MINR 7  // smallest radius on the TMEM x-window kernel (r04 A/B)
+#endif
+  if (variant == 0 && R >= SDMP_STAR_TMEM_MINR) {
+    switch (R) {
+      case 6: return launch_tmem<6, SDMP_TMEM_ROWS>(p, st, full, push);
+      case 7: return launch_tmem<7, SDMP_TMEM_ROWS>(p, st, full, push);
+      case 8: return launch_tmem<8, SDMP_TMEM_ROWS>(p, st, full, push);
+    }
+  }
+  if (variant == 0 || variant == 4) {  // 4 (tests): register-window star_tma2
     switch (R) {
       case 6: return launch_tma2<6, 16>(p, st, full, push);
       case 7: return launch_tma2<7, 16>(p, st, full, push);

@@ -146,10 +146,6 @@ __device__ __forceinline__ V2 dplane(const float* q, const float* w) {
   return acc;
 }
 
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
 // ROLE 0: tile row (g, product planes, x scatter, Laplacian, outer y / z
 // derivative, update); ROLE 1: two halo rows (g, a_y g); ROLE 2: the z-halo
 // columns of the tile rows (g, a_z g)

@@ -156,16 +156,21 @@ def test_elastic_vs_oracle(visco, so):
         assert err <= REL, (name, err, np.abs(got - want).max())
 
 
-@pytest.mark.parametrize("so", [4, 8, 12, 16])
-def test_star_kernels_bitwise_equal_generic(so, monkeypatch):
-    """star_tma (one row per warp), star_tma2 (two rows per thread, SO >= 12)
-    and the generic kernel give identical bits."""
+@pytest.mark.parametrize("so,shape", [(4, (40, 36, 44)), (8, (40, 36, 44)), (12, (40, 36, 44)),
+                                      (16, (40, 36, 44)), (14, (44, 60, 300)),
+                                      (16, (90, 80, 300))])
+def test_star_kernels_bitwise_equal_generic(so, shape, monkeypatch):
+    """star_tma (one row per warp), star_tma2 (two rows per thread, register
+    x-window, SO >= 12), star_tmem (x-window in tensor memory, SO-16) and the
+    generic kernel give identical bits; the larger shapes run several y / z
+    tiles, partial tiles and x chunks."""
     outs = []
-    for variant in ("1", "0", "3"):
+    for variant in ("1", "0", "3", "4"):
         monkeypatch.setenv("SDMP_STAR_VARIANT", variant)
         import paper_2312_13094_b200.api as A
         A._FUNCS.clear()
-        _g, u, _m, _s, rec, _dt = run_acoustic((40, 36, 44), so, 8, "diagonal", f"sb{so}_{variant}")
+        _g, u, _m, _s, rec, _dt = run_acoustic(shape, so, 8 if shape[2] < 100 else 24,
+                                               "diagonal", f"sb{so}_{variant}")
         outs.append((u.data_gather(), rec.data.copy()))
     for o in outs[1:]:
         assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
