@@ -441,10 +441,15 @@ def main():
     kernel_label = {"acoustic": (f"star_tma<{args.so // 2}> (acoustic SO-{args.so}, TMA pipeline)"
                                  if args.so < 12 else
                                  f"star_tma2<{args.so // 2}> (acoustic SO-{args.so}, TMA pipeline, "
-                                 "2 rows per thread)"),
+                                 "2 rows per thread)" if args.so < 14 else
+                                 f"star_tmem<{args.so // 2}> (acoustic SO-{args.so}, TMA pipeline, "
+                                 "2 rows per thread, x-window in tensor memory)"),
                     "damped": f"var-star stream kernel (acoustic + ABC layer, SO-{args.so})",
-                    "rotated": f"rot_g + rot_update (SPEC tti_gxx, SO-{args.so})",
-                    "tti": f"tti_g + tti_update (SO-{args.so})",
+                    "rotated": (f"rot_fused (SPEC tti_gxx, SO-{args.so}, single pass)"
+                                if args.so <= 8 else
+                                f"rot_g + rot_update (SPEC tti_gxx, SO-{args.so})"),
+                    "tti": (f"tti_fused (SO-{args.so}, single pass)" if args.so <= 6 else
+                            f"tti_g + tti_update (SO-{args.so})"),
                     "elastic": f"el_velocity / el_stress (SO-{args.so})",
                     "elastic_col": f"collocated el_velocity / el_stress (SO-{args.so})",
                     "visco": f"el_velocity / visco_stress (SO-{args.so})"}[kname]
