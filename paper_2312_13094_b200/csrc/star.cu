@@ -31,6 +31,16 @@
 
 namespace sdmp {
 
+// Front tiles are loaded with an L2 evict_last hint: R planes later the same
+// rows come back as the centre tile's interior and as the neighbouring
+// tiles' y halo.  r04 A/B (1024^3): star_tmem SO-16 +2.2% (DRAM 1.147x ->
+// 1.108x algorithmic), SO-14 +1.9%, star_tma2 SO-12 +0.5%, SO-4/8 neutral;
+// hinting the centre / pointwise tiles evict_first as well lost
+// (profiles/round2_ab_front_l2.txt).
+#ifndef SDMP_TMA_L2
+#define SDMP_TMA_L2 1
+#endif
+
 struct StarParams {
   const float* __restrict__ u0;
   const float* __restrict__ u2;
@@ -320,7 +330,11 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
         unsigned char* st = sm + s * T::STAGE;
         const bool main = i >= 2 * R;
         mbar_arrive_expect_tx(&full_bar[s], main ? main_bytes : (uint32_t)T::FRONT);
+#if SDMP_TMA_L2
+        tma_load_3d_hint(st, &tm_front, &full_bar[s], z0, y0, xa - R + i, l2_policy_evict_last());
+#else
         tma_load_3d(st, &tm_front, &full_bar[s], z0, y0, xa - R + i);
+#endif
         if (main) {
           const int x = xa + i - 2 * R;
           tma_load_3d(st + T::FRONT, &tm_center, &full_bar[s], z0 - T::OFF, y0 - R, x);
@@ -521,7 +535,11 @@ star_tma2(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ 
         unsigned char* st = sm + s * T::STAGE;
         const bool main = i >= 2 * R;
         mbar_arrive_expect_tx(&full_bar[s], main ? main_bytes : (uint32_t)T::FRONT);
+#if SDMP_TMA_L2
+        tma_load_3d_hint(st, &tm_front, &full_bar[s], z0, y0, xa - R + i, l2_policy_evict_last());
+#else
         tma_load_3d(st, &tm_front, &full_bar[s], z0, y0, xa - R + i);
+#endif
         if (main) {
           const int x = xa + i - 2 * R;
           tma_load_3d(st + T::FRONT, &tm_center, &full_bar[s], z0 - T::OFF, y0 - R, x);
@@ -731,7 +749,11 @@ star_tmem(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ 
         unsigned char* st = sm + s * T::STAGE;
         const bool main = i >= 2 * R;
         mbar_arrive_expect_tx(&full_bar[s], main ? main_bytes : (uint32_t)T::FRONT);
+#if SDMP_TMA_L2
+        tma_load_3d_hint(st, &tm_front, &full_bar[s], z0, y0, xa - R + i, l2_policy_evict_last());
+#else
         tma_load_3d(st, &tm_front, &full_bar[s], z0, y0, xa - R + i);
+#endif
         if (main) {
           const int x = xa + i - 2 * R;
           tma_load_3d(st + T::FRONT, &tm_center, &full_bar[s], z0 - T::OFF, y0 - R, x);
