@@ -46,6 +46,14 @@ __host__ __device__ constexpr int sround4(int r) { return (r + 3) & ~3; }
 #ifndef SDMP_STREAM_STAGES
 #define SDMP_STREAM_STAGES 4
 #endif
+// Front tiles are loaded with an L2 evict_last hint (their rows come back R
+// planes later as centre-tile interiors and neighbours' y halos) unless the
+// op sets kFrontL2 = false.  r04 A/B (profiles/round2_ab_front_l2.txt):
+// visco SO-16 +4.5%, elastic SO-16 +1.8%, SO-8 +1%, damped SO-16 +0.8%;
+// the TTI / rotated passes lose up to 2% and opt out.
+#ifndef SDMP_STREAM_FRONT_L2
+#define SDMP_STREAM_FRONT_L2 1
+#endif
 constexpr unsigned kHaloYZ = 0xFFFFFFFFu;
 __host__ __device__ constexpr bool halo_y(unsigned m, int c) { return (m >> (2 * c)) & 1u; }
 __host__ __device__ constexpr bool halo_z(unsigned m, int c) { return (m >> (2 * c + 1)) & 1u; }
@@ -155,6 +163,15 @@ template <class Op, int R>
 constexpr int stages_for() {
   return R >= 5 ? StagesWideOf<Op>::value : SDMP_STREAM_STAGES;
 }
+
+template <class Op, class = void>
+struct FrontL2Of {
+  static constexpr bool value = SDMP_STREAM_FRONT_L2 != 0;
+};
+template <class Op>
+struct FrontL2Of<Op, std::void_t<decltype(Op::kFrontL2)>> {
+  static constexpr bool value = SDMP_STREAM_FRONT_L2 != 0 && Op::kFrontL2;
+};
 
 template <class Op, class = void>
 struct CHaloOf {
@@ -311,8 +328,13 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
         mbar_arrive_expect_tx(&full_bar[s], main ? L::TX_MAIN : L::TX_FRONT);
         const int xf = xa - R + i;
 #pragma unroll
-        for (int f = 0; f < NF; ++f)
-          tma_load_3d(st + f * L::FRONT, &maps.m[f], &full_bar[s], z0, y0, xf);
+        for (int f = 0; f < NF; ++f) {
+          if constexpr (FrontL2Of<Op>::value)
+            tma_load_3d_hint(st + f * L::FRONT, &maps.m[f], &full_bar[s], z0, y0, xf,
+                             l2_policy_evict_last());
+          else
+            tma_load_3d(st + f * L::FRONT, &maps.m[f], &full_bar[s], z0, y0, xf);
+        }
         if (main) {
           const int x = xa + i - 2 * R;
 #pragma unroll

@@ -246,6 +246,7 @@ struct GAcc {
 #define SDMP_GOP_ROWS 1
 #endif
 struct GOp {
+  static constexpr bool kFrontL2 = false;  // r04 A/B: front L2 hint loses here
   static constexpr int NF = 2, NC = 2, NP = 3;
   static constexpr int kCtas = SDMP_GOP_CTAS;
   static constexpr int kRows = SDMP_GOP_ROWS;
@@ -284,6 +285,7 @@ struct UAcc {
 #define SDMP_UOP_VN 2
 #endif
 struct UOp {
+  static constexpr bool kFrontL2 = false;  // r04 A/B: front L2 hint loses here
   static constexpr int NF = 4, NC = 5, NP = 6;
   static constexpr int kCtas = SDMP_UOP_CTAS;
   // a_y is tapped along y only, a_z along z only: they stage one halo
@@ -317,6 +319,7 @@ struct RGAcc {
 };
 
 struct RGOp {
+  static constexpr bool kFrontL2 = false;  // r04 A/B: front L2 hint loses here
   static constexpr int NF = 1, NC = 1, NP = 3;
   static constexpr int kStagesWide = 6;  // r04 A/B (stream.cuh StagesWideOf)
   float* out;
@@ -344,6 +347,7 @@ struct RUAcc {
 };
 
 struct RUOp {
+  static constexpr bool kFrontL2 = false;  // r04 A/B: front L2 hint loses here
   static constexpr int NF = 2, NC = 3, NP = 3;
   static constexpr int kStagesWide = 6;  // r04 A/B (stream.cuh StagesWideOf)
   static constexpr unsigned kCHalo = 1u | (2u << 2) | (3u << 4);  // a_y: y, a_z: z, g: both
