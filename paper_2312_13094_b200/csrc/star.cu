@@ -21,6 +21,7 @@
 //    centre plane (star_tmem: the x-window lives in tensor memory instead).
 //    u0 is read from DRAM once (halo re-reads of neighbouring
 //    tiles hit L2), u2 and m streamed once, u1 written once: 16 B / point.
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -31,6 +32,9 @@
 
 namespace sdmp {
 
+#ifndef SDMP_STAR_TMEM_MINR
+#define SDMP_STAR_TMEM_MINR 7  // smallest radius on the TMEM x-window kernel (r04 A/B)
+#endif
 // Front tiles are loaded with an L2 evict_last hint: R planes later the same
 // rows come back as the centre tile's interior and as the neighbouring
 // tiles' y halo.  r04 A/B (1024^3): star_tmem SO-16 +2.2% (DRAM 1.147x ->
@@ -1017,6 +1021,13 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
   const bool streamable = radius[1] == R && radius[2] == R && R >= 1 && lo[2] >= round4(R) &&
                           (full[2] % 4 == 0) && (lo[2] % 4 == 0) && ((hi[2] - lo[2]) % 4 == 0) &&
                           (((uintptr_t)u0 | (uintptr_t)u1 | (uintptr_t)u2 | (uintptr_t)m) % 16 == 0);
+  if (getenv("SDMP_DEBUG"))
+    fprintf(stderr, "[sdmp] star_update R=%d box=[%ld,%ld,%ld]-[%ld,%ld,%ld] %s push=%d\n", R,
+            (long)lo[0], (long)lo[1], (long)lo[2], (long)hi[0], (long)hi[1], (long)hi[2],
+            (variant == 1 || !streamable) ? "generic"
+            : (variant == 0 && R >= SDMP_STAR_TMEM_MINR) ? "star_tmem"
+            : ((variant == 0 || variant == 4) && R >= 6) ? "star_tma2" : "star_tma",
+            push.ndir);
   // unaligned / unequal-radius boxes always take the generic kernel
   if (variant == 1 || !streamable) return launch_generic(p, st, push);
   // wide stencils: two rows per thread.  R >= 7: x-window in tensor memory
@@ -1025,9 +1036,6 @@ int star_update(cudaStream_t st, const float* u0, const float* u2, const float* 
   // the register window (0.936 vs 0.917; profiles/round2_ab_tmem.txt).
   // star_tma2: 16-row tiles (9 warps: ptxas caps registers at 168) while the
   // two x-windows fit; R = 8 needs ~210 registers, so 14-row tiles (8 warps)
-#ifndef SDMP_STAR_TMEM_MINR
-#define SDMP_STAR_TMEM_MINR 7  // smallest radius on the TMEM x-window kernel (r04 A/B)
-#endif
   if (variant == 0 && R >= SDMP_STAR_TMEM_MINR) {
     switch (R) {
       case 6: return launch_tmem<6, SDMP_TMEM_ROWS>(p, st, full, push);

@@ -117,6 +117,18 @@ def test_spec_acceptance_matrix_space_orders():
 
 
 @needs_gpu
+@pytest.mark.parametrize("nproc,topo", [(2, "2,1,1"), (4, "2,2,1")])
+def test_wide_star_kernels_multi_rank(nproc, topo):
+    """The wide acoustic kernels (star_tma2 at SO-12, star_tmem with the
+    x-window in tensor memory at SO-14/16) and the damped SO-16 op run the
+    CORE boxes with the fused halo push in full mode: multi-rank == single
+    rank bitwise in every mode."""
+    fams = "acoustic12,acoustic14,acoustic16,damped16"
+    rc, rep, err = _run(nproc, topo, "56,64,72", fams, steps=8, port=29528 + nproc)
+    _check(rc, rep, err, fams)
+
+
+@needs_gpu
 @pytest.mark.parametrize("engine", ["sm", "ce"])
 def test_halo_copy_engines(engine):
     """The alternatives to the default batched SM posts (SDMP_COPY_ENGINE=sm:
