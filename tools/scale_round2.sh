@@ -3,7 +3,7 @@
 # C4 elastic 1024^3 diagonal (+ full), C5 visco SO-16 1024^3 full.  Each line
 # carries the halo block (exposed time, bytes, link rate, NVML NVLink
 # counters).  -> gpurun_out/round2_scale/*.json + summary.txt
-O=gpurun_out/round2_scale; mkdir -p $O
+O=${SCALE_OUT:-gpurun_out/round2_scale}; mkdir -p $O
 NG=$(nvidia-smi -L | wc -l)
 run() {  # N kernel so shape mode tag
   N=$1; shift
