@@ -1078,6 +1078,10 @@ int var_star_update(cudaStream_t st, const float* u0, const float* u2, const flo
   p.u0 = u0; p.u2 = B ? u2 : nullptr; p.m = Sarr; p.u1 = u1; p.Av = A; p.Bv = B;
   p.m_is_scale = 1;
   p.A = 0.f; p.B = 0.f; p.C = 1.f;
+  if ((variant & 0xff) == 0) {  // SDMP_STAR_VARIANT=1 (tests): the generic kernel
+    const char* e = getenv("SDMP_STAR_VARIANT");
+    if (e && atoi(e) == 1) variant = 1;
+  }
   float cs = 0.f;
   for (int a = 0; a < 3; ++a) {
     SDMP_CHECK(radius[a] >= 0 && radius[a] <= SDMP_MAX_RADIUS, "radius outside 0..8");

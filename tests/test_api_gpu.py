@@ -312,6 +312,38 @@ def test_damped_acoustic_vs_oracle(so):
     assert np.any(coef["B"] > -0.999)
 
 
+@pytest.mark.parametrize("so,shape", [(4, (40, 36, 44)), (8, (40, 36, 44)), (8, (70, 80, 300)),
+                                      (16, (40, 36, 44))])
+def test_damped_kernels_bitwise_equal_generic(so, shape, monkeypatch):
+    """The variable-coefficient (damped) family: the stream-engine kernel and
+    the generic one-thread-per-point kernel give identical bits in every mode
+    (r04 A/B: a star_tma variant with per-point A, B lost 1-1.5% to the
+    engine at SO-4/8, profiles/round2_ab_damped_star.txt)."""
+    outs = []
+    for variant in ("1", "0"):
+        monkeypatch.setenv("SDMP_STAR_VARIANT", variant)
+        import paper_2312_13094_b200.api as A
+        A._FUNCS.clear()
+        grid = Grid(shape=shape, extent=tuple(10.0 * (n - 1) for n in shape))
+        kd = KD.damped_acoustic_model(grid, so=so, nbl=6, name=f"udb{so}_{variant}")
+        u, m = kd.fields["u"], kd.fields["m"]
+        steps = 12
+        dt = float(np.float32(KD.critical_dt(4.6, grid.spacing)))
+        ext = grid.extent
+        src = KD.point_source(grid, [tuple(0.5 * e + 1.3 for e in ext)], steps, dt, f0=0.030,
+                              name=f"srcdb{so}_{variant}")
+        op = Operator([kd, src.inject(u.forward, expr=src * S.DT ** 2 / m)])
+        res = []
+        for mode in ("diagonal", "full"):
+            u.data[...] = 0.0
+            op.apply(time_M=steps - 1, dt=dt, mpi=mode)
+            res.append(u.data_gather())
+        outs.append(res)
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+    assert np.abs(outs[0][0]).max() > 0
+
+
 @pytest.mark.parametrize("so", [4, 6, 8, 12])
 def test_rotated_gxx_vs_oracle(so):
     """The SPEC's tti_gxx_kernel (single-field rotated operator) through the
