@@ -448,6 +448,16 @@ static int variant_env() {
 
 #include "tti_fused.cuh"
 
+// Tile rows of the single-pass rotated operator.  With one field the
+// x-window and accumulators take half the TTI pair's registers, so 16-row
+// tiles (16 + R + 2 consumer warps at <= 80 registers, no spills) fit; the
+// g work on halo rows / columns drops from 2.25x to 1.69x at R = 4.  r04 A/B
+// (512^3): SO-6 120.4 -> 163.9 GPts/s (0.52 -> 0.71), SO-8 111.9 -> 131.9
+// (0.48 -> 0.57), SO-4 unchanged (profiles/round2_ab_rot_rows.txt).
+#ifndef SDMP_ROT_FTY
+#define SDMP_ROT_FTY 16
+#endif
+
 template <int R>
 static int launch(TTIGeneric& p, cudaStream_t st, const int64_t full[3], const Push& push) {
 #ifndef SDMP_TTI_FUSED_MAXR
@@ -576,7 +586,7 @@ static int launch_rot(TTIGeneric& p, cudaStream_t st, const int64_t full[3], con
     // single pass for the narrow stencils, as for TTI (tti_fused.cuh, NF = 1)
     const float* in[6] = {p.tap[TP], p.pnt[QP2], p.pnt[QM], p.pnt[QAX], p.pnt[QAY], p.pnt[QAZ]};
     if (variant_env() != 1 && fused_fits<R>(p.g) && tma_ok(full, in, 6))
-      return launch_fused<R, 1>(p, st, full, push);
+      return launch_fused<R, 1, SDMP_ROT_FTY>(p, st, full, push);
     dim3 b(32, 8);
     dim3 g2((p.g.hi[2] - p.g.lo[2] + 31) / 32, (p.g.hi[1] - p.g.lo[1] + 7) / 8,
             p.g.hi[0] - p.g.lo[0]);

@@ -1,7 +1,7 @@
 // Single-pass TTI for R <= 4 (SO <= 8): included by tti.cu after the
 // per-point helpers (TTICoef, dcentral, g_point, TTIGlobalAcc).
 //
-// One CTA owns an 8(y) x 64(z) tile and streams along x.  Per x-plane x' it
+// One CTA owns a TY(y) x 64(z) tile and streams along x.  Per x-plane x' it
 // evaluates g = a . grad f (f = p, r) on the tile grown by R rows (y) and
 // OFF columns (z) -- the points the outer derivative taps -- and never writes
 // g to HBM:
@@ -24,27 +24,28 @@
 //              with YZ_f = D_y(RN(a_y g_f)) + D_z(RN(a_z g_f)) (dcentral order)
 //   h0 = -acc_p (= lap - Gzz p), gzr = acc_r, then the u_point update tail.
 //
-// Warp roles: 8 tile warps (one row each, 2 z points per lane: g, the
+// Warp roles: TY tile warps (one row each, 2 z points per lane: g, the
 // accumulators, the update), R halo warps (two of the 2R halo rows each: g
-// only, a_y g stored), one z-halo warp (the 2 x OFF halo columns of the 8
-// tile rows: a_z g stored), one producer warp (TMA).
+// only, a_y g stored), TY / 8 z-halo warps (the halo columns of 8 tile rows
+// each: a_z g stored), one producer warp (TMA).  TY = 8 for the TTI pair,
+// 16 for the one-field rotated operator (SDMP_ROT_FTY, tti.cu).
 
-constexpr int kFTY = 8;   // tile rows
+constexpr int kFTY = 8;   // tile rows (TTI; the rotated operator: SDMP_ROT_FTY)
 constexpr int kFTZ = 64;  // tile columns (32 lanes x 2)
 
 // NF = 2: the TTI pair (p, r); NF = 1: the single-field rotated operator
 // (the SPEC's tti_gxx_kernel, u1 = 2 u0 - u2 + dt^2/m G u0)
-template <int R, int NF = 2>
+template <int R, int NF = 2, int TY = kFTY>
 struct FLayout {
   static constexpr int NPT = NF == 2 ? 5 : 2;  // p2 r2 m epsp delp | u2 m
   static constexpr int OFF = sround4(R);
-  static constexpr int GY = kFTY + 2 * R;   // g-region rows
+  static constexpr int GY = TY + 2 * R;     // g-region rows
   static constexpr int GZ = kFTZ + 2 * OFF; // g-region columns
-  static constexpr int CY = kFTY + 4 * R;   // centre tiles (taps of g)
+  static constexpr int CY = TY + 4 * R;     // centre tiles (taps of g)
   static constexpr int CZ = kFTZ + 4 * OFF;
   static constexpr int GREG = ((GY * GZ * 4) + 127) & ~127;
   static constexpr int CEN = ((CY * CZ * 4) + 127) & ~127;
-  static constexpr int PTB = kFTY * kFTZ * 4;
+  static constexpr int PTB = TY * kFTZ * 4;
   // stage: fronts p, r (g-region, plane x'+R) | centres p, r (plane x') |
   // a_x, a_y, a_z (g-region, plane x') | pointwise (tile, plane x'-R)
   static constexpr int O_FP = 0, O_FR = (NF - 1) * GREG, O_CP = NF * GREG;
@@ -57,7 +58,8 @@ struct FLayout {
   static constexpr int PLANE = 2 * NF * GREG;
   static constexpr int BYTES = S * STAGE + 2 * PLANE + 2 * S * 8;
   static constexpr int NHW = R;                 // halo warps (2 rows each)
-  static constexpr int NCW = kFTY + NHW + 1;    // consumer warps
+  static constexpr int NZW = TY / 8;           // z-halo warps (8 rows x 4 pairs each)
+  static constexpr int NCW = TY + NHW + NZW;    // consumer warps
   static constexpr int THREADS = 32 * (NCW + 1);
   static constexpr uint32_t TX_FRONT = NF * GY * GZ * 4;
   static constexpr uint32_t TX_G = NF * CY * CZ * 4 + 3 * GY * GZ * 4;
@@ -149,12 +151,12 @@ __device__ __forceinline__ V2 dplane(const float* q, const float* w) {
 // ROLE 0: tile row (g, product planes, x scatter, Laplacian, outer y / z
 // derivative, update); ROLE 1: two halo rows (g, a_y g); ROLE 2: the z-halo
 // columns of the tile rows (g, a_z g)
-template <int R, int ROLE, int NF>
+template <int R, int ROLE, int NF, int TY>
 __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char* plane,
                                                uint64_t* full_bar, uint64_t* empty_bar,
                                                const FusedTTI& P, const Push& push, int xa,
                                                int nit, int z0, int y0, int warp, int lane) {
-  using L = FLayout<R, NF>;
+  using L = FLayout<R, NF, TY>;
   constexpr int W = 2 * R + 1;
   constexpr int NP = ROLE == 1 ? 2 : 1;  // point pairs of this thread
   constexpr int GQ = L::GREG / 4;
@@ -164,15 +166,15 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
     gr[0] = R + warp;
     gc = L::OFF + 2 * lane;
   } else if (ROLE == 1) {
-    const int h = warp - kFTY;
+    const int h = warp - TY;
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
       const int idx = 2 * h + j;  // 0 .. 2R-1 over the halo rows
-      gr[j] = idx < R ? idx : idx + kFTY;
+      gr[j] = idx < R ? idx : idx + TY;
     }
     gc = L::OFF + 2 * lane;
   } else {
-    gr[0] = R + (lane >> 2);
+    gr[0] = R + 8 * (warp - TY - L::NHW) + (lane >> 2);
     const int cpair = lane & 3;
     gc = cpair < 2 ? (L::OFF - 4 + 2 * cpair) : (L::OFF + kFTZ + 2 * (cpair - 2));
   }
@@ -323,11 +325,11 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
   }
 }
 
-template <int R, int NF>
-__global__ void __launch_bounds__(FLayout<R, NF>::THREADS, 1)
+template <int R, int NF, int TY>
+__global__ void __launch_bounds__(FLayout<R, NF, TY>::THREADS, 1)
 tti_fused(const __grid_constant__ TMaps maps, const FusedTTI P, const int xchunk,
           const __grid_constant__ Push push) {
-  using L = FLayout<R, NF>;
+  using L = FLayout<R, NF, TY>;
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = smraw;
   unsigned char* plane = sm + L::S * L::STAGE;
@@ -344,7 +346,7 @@ tti_fused(const __grid_constant__ TMaps maps, const FusedTTI P, const int xchunk
   }
   __syncthreads();
   const int z0 = (g.lo[2] & ~3) + blockIdx.x * kFTZ;
-  const int y0 = g.lo[1] + blockIdx.y * kFTY;
+  const int y0 = g.lo[1] + blockIdx.y * TY;
   const int xa = g.lo[0] + blockIdx.z * xchunk;
   const int xb = min(xa + xchunk, g.hi[0]);
   const int nit = (xb - xa) + 4 * R;
@@ -385,14 +387,14 @@ tti_fused(const __grid_constant__ TMaps maps, const FusedTTI P, const int xchunk
     return;
   }
   // consumers: one loop per role (separate register allocations)
-  if (warp < kFTY)
-    fused_consumer<R, 0, NF>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp,
+  if (warp < TY)
+    fused_consumer<R, 0, NF, TY>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp,
                              lane);
-  else if (warp < kFTY + L::NHW)
-    fused_consumer<R, 1, NF>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp,
+  else if (warp < TY + L::NHW)
+    fused_consumer<R, 1, NF, TY>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp,
                              lane);
   else
-    fused_consumer<R, 2, NF>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp,
+    fused_consumer<R, 2, NF, TY>(sm, plane, full_bar, empty_bar, P, push, xa, nit, z0, y0, warp,
                              lane);
 }
 
@@ -498,16 +500,16 @@ __global__ void __launch_bounds__(256) rot_fused_generic(TTIGeneric p, const Pus
 
 // host: fused launch.  NF = 2 (TTI): maps {p, r | p, r | ax, ay, az | p2, r2,
 // m, epsp, delp}; NF = 1 (rotated): {u0 | u0 | ax, ay, az | u2, m}
-template <int R, int NF>
+template <int R, int NF, int TY = kFTY>
 static int launch_fused(const TTIGeneric& p, cudaStream_t st, const int64_t full[3],
                         const Push& push) {
-  using L = FLayout<R, NF>;
+  using L = FLayout<R, NF, TY>;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    SDMP_CUDA(cudaFuncSetAttribute(tti_fused<R, NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   L::BYTES));
+    SDMP_CUDA(cudaFuncSetAttribute(tti_fused<R, NF, TY>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
     attr_dev = dev;
   }
   TMaps maps;
@@ -520,7 +522,7 @@ static int launch_fused(const TTIGeneric& p, cudaStream_t st, const int64_t full
   for (int k = 0; k < NMAP; ++k) {
     const bool front = k < NF, cen = k >= NF && k < 2 * NF, am = k >= 2 * NF && k < 2 * NF + 3;
     const int bz = front || am ? L::GZ : cen ? L::CZ : kFTZ;
-    const int by = front || am ? L::GY : cen ? L::CY : kFTY;
+    const int by = front || am ? L::GY : cen ? L::CY : TY;
     int rc = make_tmap_3d(&maps.m[k], src[k], full, bz, by, k >= 2 * NF + 3);
     if (rc) return rc;
   }
@@ -530,13 +532,13 @@ static int launch_fused(const TTIGeneric& p, cudaStream_t st, const int64_t full
   f.out[1] = p.out[1];
   f.g = p.g;
   const int nz = p.g.hi[2] - p.g.lo[2], ny = p.g.hi[1] - p.g.lo[1], nx = p.g.hi[0] - p.g.lo[0];
-  const int tz = (nz + (p.g.lo[2] & 3) + kFTZ - 1) / kFTZ, ty = (ny + kFTY - 1) / kFTY;
+  const int tz = (nz + (p.g.lo[2] & 3) + kFTZ - 1) / kFTZ, ty = (ny + TY - 1) / TY;
   int nch = stream_chunks((int64_t)tz * ty, nx, 2 * R, 1);
   const int chunk = (nx + nch - 1) / nch;
   nch = (nx + chunk - 1) / chunk;
   SDMP_CHECK(nch <= 65535 && ty <= 65535, "grid too large");
   dim3 grid(tz, ty, nch), block(32, L::NCW + 1);
-  tti_fused<R, NF><<<grid, block, L::BYTES, st>>>(maps, f, chunk, push);
+  tti_fused<R, NF, TY><<<grid, block, L::BYTES, st>>>(maps, f, chunk, push);
   SDMP_LAUNCHED();
   return SDMP_OK;
 }
