@@ -232,6 +232,10 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
           g_point<R>(a, P.c, gp, grv);
         else
           gp = g1_point<R>(a, P.c);
+        // the Laplacian taps of p are g's taps: form it before the product
+        // stores so the shared-memory loads are reused, not repeated (r04 A/B:
+        // TTI SO-4 +3%, SO-6 +5%; profiles/round2_ab_fused_lapfirst.txt)
+        if constexpr (ROLE == 0 && NF == 2) lapv = lap_point<R>(a, P.c);
         if (ROLE != 2) {  // a_y g: tapped along y (tile and halo rows)
           *reinterpret_cast<uint64_t*>(pl + o) = vmul(a.ay, gp).r;
           if (NF == 2) *reinterpret_cast<uint64_t*>(pl + GQ + o) = vmul(a.ay, grv).r;
@@ -251,7 +255,6 @@ __device__ __forceinline__ void fused_consumer(unsigned char* sm, unsigned char*
             accp[u + k] = vcfma(cj, axp, accp[u + k]);
             if (NF == 2) accr[u + k] = vcfma(cj, axr, accr[u + k]);
           }
-          if (NF == 2) lapv = lap_point<R>(a, P.c);
         }
       }
     }
