@@ -503,7 +503,8 @@ def main():
         torch.cuda.synchronize()
         ms_c = ctx.allreduce_max(e0.elapsed_time(e1))
         posts = [(i, a) for i, a in enumerate(ep.actions) if a.kind == "post" and a.messages]
-        sent = sum(m.volume * len(a.spot.fields) for _i, a in posts for m in a.messages) * 4
+        sent = sum(m.volume * sum(a.spot.sends(f, t, m.direction) for f, t in a.spot.fields)
+                   for _i, a in posts for m in a.messages) * 4
         post_ms = sum(rows[plan.native_index[i]][4] for i, _a in posts)
         fused = any(a.pushed for _i, a in posts)
         if fused:

@@ -289,11 +289,17 @@ class StaggeredPhase:
     def radius(self):
         return (self.so // 2,) * 3
 
+    # axes each stress is differentiated along by the velocity update
+    # (tau = xx, yy, zz, xy, xz, yz; PAPER.md:1041-1051, SPEC.md:587-592:
+    # v_i,t = b sum_j D_j tau_ij)
+    TAU_AXES = ((0,), (1,), (2,), (0, 1), (0, 2), (1, 2))
+
     def reads(self):
         r, zero = self.radius, (0, 0, 0)
         if self.kind == "v":
-            return ([(f, 0, r) for f in self.tau] + [(f, 0, zero) for f in self.v]
-                    + [(self.params[0], 0, zero)])
+            tau = [(f, 0, tuple(r[a] if a in ax else 0 for a in range(3)))
+                   for f, ax in zip(self.tau, self.TAU_AXES)]
+            return tau + [(f, 0, zero) for f in self.v] + [(self.params[0], 0, zero)]
         out = [(f, 1, r) for f in self.v] + [(f, 0, zero) for f in self.tau]
         out += [(f, 0, zero) for f in self.mem] + [(f, 0, zero) for f in self.params]
         return out
@@ -854,10 +860,24 @@ def align_accesses(eq: S.StencilEquation, halo=None) -> S.StencilEquation:
 
 @dataclass
 class HaloSpot:
-    """Exchange of ``fields`` (spec, tshift) with per-axis ``radius``."""
+    """Exchange of ``fields`` (spec, tshift) with per-axis ``radius`` (the
+    union over the fields: it sizes CORE / OWNED and the message boxes).
+
+    ``field_radius`` holds each field's own per-axis read radius, as Devito's
+    HaloScheme keeps one per function: a field read with offsets along x
+    only (the staggered velocity update reads txx only through D_x) never
+    ships its y faces or xy corners."""
 
     fields: List[Tuple[S.FieldSpec, int]]
     radius: Tuple[int, ...]
+    field_radius: Optional[Dict[Tuple[S.FieldSpec, int], Tuple[int, ...]]] = None
+
+    def sends(self, f: S.FieldSpec, t: int, direction) -> bool:
+        """Whether ``(f, t)`` travels in the message along ``direction``:
+        every axis the direction crosses must be one the field is read
+        along."""
+        fr = (self.field_radius or {}).get((f, t), self.radius)
+        return all(fr[a] > 0 for a, d in enumerate(direction) if d)
 
 
 @dataclass
@@ -888,7 +908,7 @@ def halo_phases(kernels: Sequence, nranks: int) -> HaloAnalysis:
     phases = []
     count = 0
     for k in kernels:
-        need, rad = [], None
+        need, rad, frad = [], None, {}
         for f, t, r in k.reads():
             nd = len(r)
             if not any(r) or nranks == 1:
@@ -902,9 +922,11 @@ def halo_phases(kernels: Sequence, nranks: int) -> HaloAnalysis:
                 if (f, t) not in [x[0:2] for x in need]:
                     need.append((f, t))
                 rad = tuple(max(a, b) for a, b in zip(rad or r, r))
+                fr = frad.get((f, t))
+                frad[(f, t)] = tuple(max(a, b) for a, b in zip(fr or r, r))
         spot = None
         if need:
-            spot = HaloSpot(need, rad)
+            spot = HaloSpot(need, rad, frad)
             count += 1
             for ft in need:
                 dirty.discard(ft)
@@ -1022,11 +1044,12 @@ def _fuse_pushes(acts, analysis: HaloAnalysis, decomp, rank: int) -> None:
     pushed).  Falls back to copies if any precondition fails."""
     from .distfield import RegionName, diagonal_messages, rank_regions
 
-    radius = {}
+    radius, spot_of = {}, {}
     for ph in analysis.phases:
         if ph.halo is not None:
-            for f, _t in ph.halo.fields:
+            for f, t in ph.halo.fields:
                 radius[f] = ph.halo.radius
+                spot_of[f] = (ph.halo, t)
     if not radius:
         return
     geo = {f: diagonal_messages(decomp, rank, r) for f, r in radius.items()}
@@ -1063,8 +1086,12 @@ def _fuse_pushes(acts, analysis: HaloAnalysis, decomp, rank: int) -> None:
                         return
         elif a.kind == "inject" and a.sparse.field in radius:
             plan.append((a, ([a.sparse.field], geo[a.sparse.field])))
-    for a, push in plan:
-        a.push = push
+    for a, (outs, msgs) in plan:
+        # per output and direction: does the neighbour read this field
+        # across that face (HaloSpot.sends)?  Kernels skip the others.
+        sends = [[spot_of[f][0].sends(f, spot_of[f][1], m.direction) for m in msgs]
+                 for f in outs]
+        a.push = (outs, msgs, sends)
     for a in acts:
         if a.kind == "post":
             a.pushed = True

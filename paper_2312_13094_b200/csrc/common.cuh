@@ -95,7 +95,8 @@ __device__ __forceinline__ void push_point(const Push& P, int x, int y, int z, c
     if (!push_in(g, x, y, z)) continue;
     const int64_t j = (int64_t)(x + g.off[0]) * g.psx + (int64_t)(y + g.off[1]) * g.psy +
                       (z + g.off[2]);
-    for (int q = 0; q < nv && q < P.nout; ++q) P.base[q][d][j] = vals[q];
+    for (int q = 0; q < nv && q < P.nout; ++q)
+      if (P.base[q][d]) P.base[q][d][j] = vals[q];
   }
 }
 

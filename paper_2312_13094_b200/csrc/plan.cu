@@ -179,15 +179,19 @@ int parse_push(const sdmp_plan* p, const Action& a, int64_t time, Push* out) {
       g.hi[k] = (int)gp[9 * d + 3 + k];
       g.off[k] = (int)gp[9 * d + 6 + k];
     }
-    const int64_t pf = fid[d];  // output 0 of direction d
-    SDMP_CHECK(pf >= 0 && pf < (int64_t)p->fields.size(), "push field id");
-    g.psy = p->fields[pf].full[2];
-    g.psx = p->fields[pf].full[1] * p->fields[pf].full[2];
+    // field id -1: the neighbour never reads output q across this face
+    // (per-field halo radii, compiler.HaloSpot.sends); the kernels skip a
+    // null base.  Strides come from the first output that is sent.
+    int64_t pf = -1;
     for (int q = 0; q < nout; ++q) {
       const int64_t f = fid[q * ndir + d];
-      SDMP_CHECK(f >= 0 && f < (int64_t)p->fields.size(), "push field id");
-      out->base[q][d] = resolve(p, f, tsh, time);
+      SDMP_CHECK(f >= -1 && f < (int64_t)p->fields.size(), "push field id");
+      out->base[q][d] = f >= 0 ? resolve(p, f, tsh, time) : nullptr;
+      if (pf < 0) pf = f;
     }
+    SDMP_CHECK(pf >= 0, "push direction without any field");
+    g.psy = p->fields[pf].full[2];
+    g.psx = p->fields[pf].full[1] * p->fields[pf].full[2];
   }
   const int64_t lf = a.i[2];  // first field of the action: this rank's layout
   out->msy = p->fields[lf].full[2];

@@ -257,6 +257,7 @@ __device__ __forceinline__ void push_vals(const Push& P, int x, int y, int z, co
     const int64_t j = (int64_t)(x + g.off[0]) * g.psx + (int64_t)(y + g.off[1]) * g.psy +
                       (z + g.off[2]);
     for (int q = 0; q < n && q < P.nout; ++q) {
+      if (!P.base[q][d]) continue;  // not read across this face
       float* dst = P.base[q][d] + j;
       if (in0 && in1 && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
         *reinterpret_cast<uint64_t*>(dst) = v[q].r;

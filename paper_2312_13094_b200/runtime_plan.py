@@ -256,19 +256,26 @@ class NativeOperatorPlan:
         HALO (same buffer rotation, tshift +1)."""
         if a.push is None:
             return []
-        outs, msgs = a.push
+        outs, msgs, sends = a.push
+        # directions no output crosses are dropped (per-field halo radii)
+        keep = [d for d in range(len(msgs)) if any(fs[d] for fs in sends)]
+        msgs = [msgs[d] for d in keep]
+        sends = [[fs[d] for d in keep] for fs in sends]
+        if not msgs:
+            return []
         fn = self.op.fields[outs[0]]
         h = fn.halo3
-        nd = len(msgs[0].send[0]) if msgs else 3
+        nd = len(msgs[0].send[0])
         ints = [self.PUSH_MAGIC, len(msgs), len(outs), 1]
         for m in msgs:
             lo = [l + hh for l, hh in zip(m.send[0], h)] + [0] * (3 - nd)
             hi = [u + hh for u, hh in zip(m.send[1], h)] + [1] * (3 - nd)
             off = [r - s_ for r, s_ in zip(m.recv[0], m.send[0])] + [0] * (3 - nd)
             ints += lo + hi + off
-        for f in outs:
-            for m in msgs:
-                ints.append(self.pfid[(m.peer, f)])
+        for f, fs in zip(outs, sends):
+            for m, s_ in zip(msgs, fs):
+                # -1: the neighbour never reads f across this face (no store)
+                ints.append(self.pfid[(m.peer, f)] if s_ else -1)
         return ints
 
     def _post_ints(self, a, fid, pfid, pflag, decomp, rank):
@@ -290,6 +297,8 @@ class NativeOperatorPlan:
         n = 0
         for m in a.messages:
             for f, t in a.spot.fields:
+                if not a.spot.sends(f, t, m.direction):
+                    continue  # f is not read across this face (HaloSpot.field_radius)
                 fn = self.op.fields[f]
                 slo = [l + h for l, h in zip(m.send[0], fn.halo3)] + [0] * (3 - len(m.send[0]))
                 ext = [u - l for l, u in zip(*m.send)] + [1] * (3 - len(m.send[0]))

@@ -89,6 +89,50 @@ def test_elastic_two_exchanges_per_step():
     assert [x[1] for x in an.phases[1].halo.fields] == [1] * 3   # v[t1] before tau
 
 
+@pytest.mark.parametrize("collocated", [False, True])
+def test_stress_halos_only_along_their_derivative_axes(collocated):
+    """Per-field halo radii (Devito's per-function HaloScheme): the velocity
+    update reads each stress only along the axes it differentiates it
+    (v_i,t = b sum_j D_j tau_ij), so txx ships x faces only, tyy y faces
+    only, tzz none (z is never split), shears their two axes; velocities
+    every face.  Posts and fused pushes carry exactly those (field, face)
+    pairs, which cuts a (2,2,1) rank's stress halo bytes in half."""
+    g = S.GridSpec((32,) * 3, (150.0,) * 3)
+    v = tuple(S.FieldSpec(n, g, 8, 1) for n in ("vx", "vy", "vz"))
+    t = tuple(S.FieldSpec(n, g, 8, 1) for n in ("txx", "tyy", "tzz", "txy", "txz", "tyz"))
+    b, lam, mu = (S.FieldSpec(n, g, 8, 0) for n in ("b", "lam", "mu"))
+    kv = CP.StaggeredPhase("v", v, t, (b,), so=8, collocated=collocated)
+    kt = CP.StaggeredPhase("t", v, t, (lam, mu), so=8, collocated=collocated)
+    d = DC.Decomposition.create((64, 64, 32), 4, (2, 2, 1))
+    an = CP.halo_phases([kv, kt], d.nranks)
+    spot_t, spot_v = an.phases[0].halo, an.phases[1].halo
+    assert spot_t.radius == (4, 4, 4)
+    faces = {"x": (1, 0, 0), "y": (0, 1, 0), "xy": (1, 1, 0)}
+    want = {"txx": {"x"}, "tyy": {"y"}, "tzz": set(), "txy": {"x", "y", "xy"},
+            "txz": {"x"}, "tyz": {"y"}}
+    for f, tt in spot_t.fields:
+        got = {k for k, dvec in faces.items() if spot_t.sends(f, tt, dvec)}
+        assert got == want[f.name], f.name
+    assert all(spot_v.sends(f, tt, dvec) for f, tt in spot_v.fields for dvec in faces.values())
+    for mode in ("diagonal", "full"):
+        p = CP.lower_mode(an, d, 0, mode)
+        post = [a for a in p.actions if a.kind == "post"][0]
+        full_vol = sum(m.volume * len(post.spot.fields) for m in post.messages)
+        sent = sum(m.volume * sum(post.spot.sends(f, tt, m.direction)
+                                  for f, tt in post.spot.fields) for m in post.messages)
+        # rank 0 of (2,2,1): one x face, one y face, one corner per field
+        assert 2 * sent < full_vol
+        if mode == "full":
+            slabs = [a for a in p.actions if a.kind == "compute" and a.region == "OWNED"
+                     and a.kernel is kt]
+            assert slabs
+            for a in slabs:
+                outs, msgs, sends = a.push
+                for f, fs in zip(outs, sends):
+                    for m, s_ in zip(msgs, fs):
+                        assert s_ == spot_t.sends(f, 0, m.direction)
+
+
 def plan_for(mode, dims=(2, 2, 1), rank=0, shape=(32, 32, 32)):
     eq, u, m = acoustic_eq(8, 3, 32)
     k = CP.recognise([eq])[0]

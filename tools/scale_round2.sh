@@ -5,8 +5,9 @@
 # counters).  -> gpurun_out/round2_scale/*.json + summary.txt
 O=${SCALE_OUT:-gpurun_out/round2_scale}; mkdir -p $O
 NG=$(nvidia-smi -L | wc -l)
-run() {  # N kernel so shape mode tag
+run() {  # N kernel so shape mode tag   (ONLY=<regex>: run matching tags only)
   N=$1; shift
+  if [ -n "$ONLY" ] && ! echo "$5" | grep -Eq "$ONLY"; then return; fi
   L="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2961$N"
   if [ "$N" = 2 ]; then export CUDA_VISIBLE_DEVICES=0,1; else unset CUDA_VISIBLE_DEVICES; fi
   shp=""; [ "$3" != "-" ] && shp="--shape $3"
