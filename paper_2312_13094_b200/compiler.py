@@ -22,6 +22,7 @@ path:
 """
 from __future__ import annotations
 
+import os
 import random
 from dataclasses import dataclass, field
 from fractions import Fraction
@@ -876,6 +877,8 @@ class HaloSpot:
         """Whether ``(f, t)`` travels in the message along ``direction``:
         every axis the direction crosses must be one the field is read
         along."""
+        if os.environ.get("SDMP_FIELD_RADII", "1") == "0":  # A/B: every face
+            return True
         fr = (self.field_radius or {}).get((f, t), self.radius)
         return all(fr[a] > 0 for a, d in enumerate(direction) if d)
 
