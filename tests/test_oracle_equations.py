@@ -9,8 +9,8 @@ view shifted by its offsets, dt and h_a to numbers (``eval_numeric``) -- and
 compared with the oracle step on the same fp64 arrays with exact (unrounded)
 FD weights.  The GPU kernels are compared with this oracle in the -m gpu
 suite, so the chain reference equations -> oracle -> CUDA is closed for
-acoustic, TTI (two-field, nested derivatives), the rotated G_xx operator and
-the collocated elastic system.  CPU only, seconds."""
+acoustic, damped acoustic, TTI (two-field, nested derivatives), the rotated
+G_xx operator and the collocated elastic system.  CPU only, seconds."""
 import numpy as np
 import pytest
 
@@ -140,3 +140,32 @@ def test_oracle_collocated_elastic_equals_solved_equations(so):
                     arrays[("lam", 0)], arrays[("mu", 0)], sc, DT, box, t1, col=True)
     for i in range(6):
         _close(t1[i][K._sl(box)], _eval(eqs[3 + i], arrays, box, g.spacing))
+
+
+@pytest.mark.parametrize("so", [4, 8])
+def test_oracle_damped_equals_solved_equation(so):
+    """Acoustic with an absorbing layer, ``m*u.dt2 - u.laplace + damp*u.dt``
+    solved by the reference's solve_forward: the oracle's var-star update
+    with the closed-form A = (2m + d dt)/(m + d dt), B = -m/(m + d dt),
+    S = dt^2/(m + d dt) equals the solved rhs, and so do the coefficients the
+    product binds from the equation (compiler.VarStarKernel.coefficients)."""
+    g = _grid()
+    u, m, dmp = (S.FieldSpec("u", g, so, 2), S.FieldSpec("m", g, so, 0),
+                 S.FieldSpec("damp", g, so, 0))
+    eq = S.solve_forward(S.Eq(m.at() * u.dt2 - u.laplace + dmp.at() * u.dt), u.forward)
+    arrays, box = _setup(so, [("u", 0), ("u", -1), ("m", 0), ("damp", 0)], 5)
+    arrays[("m", 0)] = 0.2 + np.abs(arrays[("m", 0)])
+    arrays[("damp", 0)] = np.abs(arrays[("damp", 0)])
+    M, D = arrays[("m", 0)], arrays[("damp", 0)]
+    A, B, Sc = (2 * M + D * DT) / (M + D * DT), -M / (M + D * DT), DT * DT / (M + D * DT)
+    want = _eval(eq, arrays, box, g.spacing)
+    lap = _weights(2, so, g.spacing)
+    out = np.zeros_like(M)
+    K.var_star_update(arrays[("u", 0)], arrays[("u", -1)], A, B, Sc, lap, box, out)
+    _close(out[K._sl(box)], want)
+    k = CP.recognise([eq])[0]
+    assert isinstance(k, CP.VarStarKernel)
+    s = K._sl(box)
+    Ak, Bk, Sk = k.coefficients({m: M[s], dmp: D[s]}, DT, g.spacing)
+    for got, ref in ((Ak, A[s]), (Bk, B[s]), (Sk, Sc[s])):
+        _close(np.asarray(got), ref)
