@@ -1127,7 +1127,6 @@ def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
     def kernel_writes_field(k, spec):
         return any(f == spec for f, _t in k.writes())
 
-    prev_full = None  # (OWNED event, radius, fields written, injects) of a full phase
     for pi, ph in enumerate(analysis.phases):
         k = ph.kernel
         spot = ph.halo
@@ -1141,22 +1140,10 @@ def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
             # the injection) wrote on stream 0, and the peer's flag does not
             # order them (found by the full-size bitwise check, r02)
             acts.append(Action("record", 0, event=ev))
-            # full mode, early flag release: when every field of this spot
-            # was written by the previous phase, whose OWNED slabs (stream 1)
-            # cover this spot's send boxes and which injects nothing, the
-            # post depends only on those slabs -- not on the previous CORE.
-            # A neighbour's OWNED slabs then wait for this rank's slabs, not
-            # for its whole previous phase (cross-rank coupling through CORE
-            # removed; the next-step boundary keeps the full join).
-            early = (mode == "full" and prev_full is not None and not prev_full[3]
-                     and {f for f, _t in spot.fields} <= prev_full[2]
-                     and all(a <= b for a, b in zip(spot.radius, prev_full[1]))
-                     and os.environ.get("SDMP_EARLY_POST", "1") != "0")
-            acts.append(Action("streamwait", 2, event=prev_full[0] if early else ev))
+            acts.append(Action("streamwait", 2, event=ev))
             if mode == "full":
                 acts.append(Action("streamwait", 1, event=ev))
             ev += 1
-        prev_full = None
         if spot is None:
             # no exchange: the interpolation reads the field's current
             # buffer, which this phase's update does not write (explicit
@@ -1213,8 +1200,6 @@ def lower_mode(analysis: HaloAnalysis, decomp, rank: int, mode: str,
                 acts.append(Action("compute", 1, kernel=k, box=slab, region="OWNED"))
             acts.append(Action("record", 1, event=ev))
             acts.append(Action("streamwait", 0, event=ev))
-            prev_full = (ev, spot.radius, {f for f, t in k.writes() if t == 1},
-                         bool(my_injects))
             ev += 1
         for t in my_injects:
             acts.append(Action("inject", 0, sparse=t))
