@@ -60,7 +60,7 @@ def _close(a, b):
     assert np.abs(a - b).max() <= 1e-11 * scale, np.abs(a - b).max() / scale
 
 
-@pytest.mark.parametrize("so", [4, 8])
+@pytest.mark.parametrize("so", [2, 4, 8, 12, 16])
 def test_oracle_acoustic_equals_solved_equation(so):
     g = _grid()
     u, m = S.FieldSpec("u", g, so, 2), S.FieldSpec("m", g, so, 0)
@@ -73,7 +73,7 @@ def test_oracle_acoustic_equals_solved_equation(so):
     _close(out[K._sl(box)], _eval(eq, arrays, box, g.spacing))
 
 
-@pytest.mark.parametrize("so", [4, 8])
+@pytest.mark.parametrize("so", [4, 8, 16])
 def test_oracle_tti_equals_solved_equations(so):
     """The two-field TTI pair as nested Deriv(a * Deriv)
     equations (compiler.tti_updates, pinned to the reference by sha256)."""
@@ -97,7 +97,7 @@ def test_oracle_tti_equals_solved_equations(so):
     _close(r1[K._sl(box)], _eval(eq_r, arrays, box, g.spacing))
 
 
-@pytest.mark.parametrize("so", [4, 8])
+@pytest.mark.parametrize("so", [4, 8, 16])
 def test_oracle_rotated_equals_solved_equation(so):
     """The SPEC's tti_gxx_kernel from compiler.rotated_update."""
     g = _grid()
@@ -114,7 +114,7 @@ def test_oracle_rotated_equals_solved_equation(so):
     _close(out[K._sl(box)], _eval(eq, arrays, box, g.spacing))
 
 
-@pytest.mark.parametrize("so", [4, 8])
+@pytest.mark.parametrize("so", [2, 4, 8, 16])
 def test_oracle_collocated_elastic_equals_solved_equations(so):
     """The SPEC's elastic_kernel as nine first-order
     updates (compiler.elastic_updates): the oracle's velocity phase against
@@ -142,7 +142,7 @@ def test_oracle_collocated_elastic_equals_solved_equations(so):
         _close(t1[i][K._sl(box)], _eval(eqs[3 + i], arrays, box, g.spacing))
 
 
-@pytest.mark.parametrize("so", [4, 8])
+@pytest.mark.parametrize("so", [4, 8, 16])
 def test_oracle_damped_equals_solved_equation(so):
     """Acoustic with an absorbing layer, ``m*u.dt2 - u.laplace + damp*u.dt``
     solved by the reference's solve_forward: the oracle's var-star update
@@ -169,3 +169,21 @@ def test_oracle_damped_equals_solved_equation(so):
     Ak, Bk, Sk = k.coefficients({m: M[s], dmp: D[s]}, DT, g.spacing)
     for got, ref in ((Ak, A[s]), (Bk, B[s]), (Sk, Sc[s])):
         _close(np.asarray(got), ref)
+
+
+@pytest.mark.parametrize("so,nd", [(2, 2), (4, 2), (2, 3), (8, 3)])
+def test_oracle_diffusion_equals_solved_equation(so, nd):
+    """``Eq(u.dt, u.laplace)`` (Listing 1/4): forward
+    Euler u1 = u0 + dt L(u0), in 2D and 3D."""
+    shape, extent = SHAPE[:nd], EXTENT[:nd]
+    g = S.GridSpec(shape, extent)
+    u = S.FieldSpec("u", g, so, 1)
+    eq = S.solve_forward(S.Eq(u.dt, u.laplace), u.forward)
+    rng = np.random.default_rng(6)
+    full = tuple(n + 2 * so for n in shape)
+    box = ((so,) * nd, tuple(so + n for n in shape))
+    arrays = {("u", 0): rng.standard_normal(full)}
+    out = np.zeros(full)
+    K.star_update(arrays[("u", 0)], None, None, _weights(2, so, g.spacing), 1.0, 0.0, DT,
+                  box, out)
+    _close(out[K._sl(box)], _eval(eq, arrays, box, g.spacing))
