@@ -365,7 +365,10 @@ static int launch_el_stream(const Op& op, const Geom& g, const int64_t full[3],
 #ifndef SDMP_VISCO_TYN
 #define SDMP_VISCO_TYN 16
 #endif
-  constexpr int TYN = vel ? SDMP_VEL_TYN : (visco ? SDMP_VISCO_TYN : 8);
+#ifndef SDMP_STRESS_TYN
+#define SDMP_STRESS_TYN 8
+#endif
+  constexpr int TYN = vel ? SDMP_VEL_TYN : (visco ? SDMP_VISCO_TYN : SDMP_STRESS_TYN);
 #ifndef SDMP_STRESS_TYW
 #define SDMP_STRESS_TYW 8
 #endif
