@@ -71,39 +71,6 @@ inline int make_geom(const int64_t full[3], const int64_t lo[3], const int64_t h
 // (x, y, z) + off in the peer's FULL array with strides (psx, psy, 1).
 constexpr int kPushDirs = 8;
 constexpr int kPushOut = 12;
-// CTA rasterisation of the (z-tile, y-tile) grid of the streaming kernels.
-// The hardware dispatches CTAs in linear block order, so with plain order a
-// wave of resident CTAs covers whole z rows of tiles for a few y rows and the
-// next wave re-reads the y-halo rows along its edge from DRAM.  With
-// SDMP_SWZ = W > 0, consecutive CTAs cover bands of W z-tiles x all y-tiles
-// (the last band narrower), so a wave is squarer in tile space and its
-// y-perimeter shorter.  Bijective; W = 0 keeps the plain order.
-#ifndef SDMP_SWZ
-#define SDMP_SWZ 0
-#endif
-__device__ __forceinline__ void tile_xy(int& bx, int& by) {
-  const int nx = (int)gridDim.x, ny = (int)gridDim.y;
-  if (SDMP_SWZ <= 0 || nx <= SDMP_SWZ) {
-    bx = (int)blockIdx.x;
-    by = (int)blockIdx.y;
-    return;
-  }
-  const int W = SDMP_SWZ;
-  const int L = (int)blockIdx.x + (int)blockIdx.y * nx;
-  const int nfull = nx / W;
-  const int band = L / (W * ny);
-  if (band < nfull) {
-    const int r = L - band * W * ny;
-    bx = band * W + r % W;
-    by = r / W;
-  } else {
-    const int w = nx - nfull * W;
-    const int r = L - nfull * W * ny;
-    bx = nfull * W + r % w;
-    by = r / w;
-  }
-}
-
 struct PushGeo {
   int lo[3], hi[3], off[3];
   int64_t psx, psy;

@@ -316,10 +316,8 @@ star_tma(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ C
     fence_barrier_init();
   }
   __syncthreads();
-  int bx, by;
-  tile_xy(bx, by);
-  const int z0 = p.g.lo[2] + bx * kTZ;
-  const int y0 = p.g.lo[1] + by * TY;
+  const int z0 = p.g.lo[2] + blockIdx.x * kTZ;
+  const int y0 = p.g.lo[1] + blockIdx.y * TY;
   const int xa = p.g.lo[0] + blockIdx.z * xchunk;
   const int xb = min(xa + xchunk, p.g.hi[0]);
   const int nit = (xb - xa) + 2 * R;
@@ -523,10 +521,8 @@ star_tma2(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ 
     fence_barrier_init();
   }
   __syncthreads();
-  int bx, by;
-  tile_xy(bx, by);
-  const int z0 = p.g.lo[2] + bx * kTZ;
-  const int y0 = p.g.lo[1] + by * TY;
+  const int z0 = p.g.lo[2] + blockIdx.x * kTZ;
+  const int y0 = p.g.lo[1] + blockIdx.y * TY;
   const int xa = p.g.lo[0] + blockIdx.z * xchunk;
   const int xb = min(xa + xchunk, p.g.hi[0]);
   const int nit = (xb - xa) + 2 * R;
@@ -739,10 +735,8 @@ star_tmem(const __grid_constant__ CUtensorMap tm_front, const __grid_constant__ 
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  int bx, by;
-  tile_xy(bx, by);
-  const int z0 = p.g.lo[2] + bx * kTZ;
-  const int y0 = p.g.lo[1] + by * TY;
+  const int z0 = p.g.lo[2] + blockIdx.x * kTZ;
+  const int y0 = p.g.lo[1] + blockIdx.y * TY;
   const int xa = p.g.lo[0] + blockIdx.z * xchunk;
   const int xb = min(xa + xchunk, p.g.hi[0]);
   const int nit = (xb - xa) + 2 * R;

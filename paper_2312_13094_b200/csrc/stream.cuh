@@ -313,10 +313,8 @@ stream_kernel(const __grid_constant__ TMaps maps, const Op op, const Geom g, con
   __syncthreads();
   // TMA boxes must start on a 16 B boundary along z: tiles are aligned down
   // to a multiple of 4 floats and lanes outside the box are masked off.
-  int bx, by;
-  tile_xy(bx, by);
-  const int z0 = (g.lo[2] & ~3) + bx * L::TZ;
-  const int y0 = g.lo[1] + by * TY;
+  const int z0 = (g.lo[2] & ~3) + blockIdx.x * L::TZ;
+  const int y0 = g.lo[1] + blockIdx.y * TY;
   const int xa = g.lo[0] + blockIdx.z * xchunk;
   const int xb = min(xa + xchunk, g.hi[0]);
   const int nit = (xb - xa) + 2 * R;

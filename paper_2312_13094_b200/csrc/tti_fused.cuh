@@ -348,10 +348,8 @@ tti_fused(const __grid_constant__ TMaps maps, const FusedTTI P, const int xchunk
     fence_barrier_init();
   }
   __syncthreads();
-  int bx, by;
-  tile_xy(bx, by);
-  const int z0 = (g.lo[2] & ~3) + bx * kFTZ;
-  const int y0 = g.lo[1] + by * TY;
+  const int z0 = (g.lo[2] & ~3) + blockIdx.x * kFTZ;
+  const int y0 = g.lo[1] + blockIdx.y * TY;
   const int xa = g.lo[0] + blockIdx.z * xchunk;
   const int xb = min(xa + xchunk, g.hi[0]);
   const int nit = (xb - xa) + 4 * R;
