@@ -114,6 +114,12 @@ def test_stress_halos_only_along_their_derivative_axes(collocated):
         got = {k for k, dvec in faces.items() if spot_t.sends(f, tt, dvec)}
         assert got == want[f.name], f.name
     assert all(spot_v.sends(f, tt, dvec) for f, tt in spot_v.fields for dvec in faces.values())
+    # basic: the x step ships txx, txy, txz; the y step tyy, txy, tyz
+    posts = [a for a in CP.lower_mode(an, d, 0, "basic").actions
+             if a.kind == "post" and a.spot is spot_t]
+    shipped = [{f.name for f, tt in a.spot.fields
+                if any(a.spot.sends(f, tt, m.direction) for m in a.messages)} for a in posts]
+    assert shipped[:2] == [{"txx", "txy", "txz"}, {"tyy", "txy", "tyz"}]
     for mode in ("diagonal", "full"):
         p = CP.lower_mode(an, d, 0, mode)
         post = [a for a in p.actions if a.kind == "post"][0]
